@@ -1,0 +1,176 @@
+"""ORACLE — TEST INFRASTRUCTURE ONLY.
+
+Plain, slow, unfused CPU reference for the fused element-wise expression +
+reduction path (see coot_oracle.c for the per-function paper citations).
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s
+``cpu_baseline`` / ``--impl reference`` legs may import this package; the
+product package ``paper_2508_11385_b200`` never does, and shares no code
+with it.
+
+Programs are lists of ``(op_name, arg)`` tuples in postfix order, e.g.
+``[("LOAD", 0), ("LOAD", 1), ("MUL", 0), ("EXP", 0), ("SCALAR", 0),
+("LOAD", 2), ("MUL", 0), ("ADD", 0)]`` for ``exp(A % B) + 3*C``.
+Arrays are numpy 1-D arrays holding the column-major element order.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+from . import build as _build
+
+TYPES = {"f32": 0, "f64": 1, "u32": 2, "s64": 3}
+DTYPES = {"f32": np.float32, "f64": np.float64, "u32": np.uint32, "s64": np.int64}
+OPS = {
+    "LOAD": 0, "SCALAR": 1, "NEG": 2, "ABS": 3, "SQUARE": 4, "SQRT": 5, "EXP": 6,
+    "LOG": 7, "ADD": 8, "SUB": 9, "MUL": 10, "DIV": 11, "MIN": 12, "MAX": 13,
+}
+KINDS = {"ACCU": 0, "MIN": 1, "MAX": 2, "MINMAX": 3, "NORM2": 4}
+FILLS = {"randu": 0, "ones": 1, "iota": 2, "modk": 3, "colidx": 4, "rowidx": 5, "zeros": 6}
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        path = _build.build()
+        L = ctypes.CDLL(path)
+        u64, i32, vp = ctypes.c_uint64, ctypes.c_int, ctypes.c_void_p
+        L.orc_hash.restype = u64
+        L.orc_hash.argtypes = [u64, u64, u64]
+        L.orc_fill.restype = i32
+        L.orc_fill.argtypes = [i32, i32, u64, u64, u64, u64, u64, u64, vp]
+        L.orc_eval.restype = i32
+        L.orc_eval.argtypes = [i32, u64, ctypes.POINTER(vp), i32, vp, i32,
+                               ctypes.POINTER(i32), ctypes.POINTER(i32), i32, vp]
+        L.orc_acc_size.restype = ctypes.c_size_t
+        L.orc_acc_init.restype = i32
+        L.orc_acc_init.argtypes = [vp, i32, i32]
+        L.orc_acc_add.restype = i32
+        L.orc_acc_add.argtypes = [vp, u64, vp]
+        L.orc_acc_final.restype = i32
+        L.orc_acc_final.argtypes = [vp, vp]
+        L.orc_reduce.restype = i32
+        L.orc_reduce.argtypes = [i32, i32, u64, vp, vp]
+        L.orc_sum_dim.restype = i32
+        L.orc_sum_dim.argtypes = [i32, i32, u64, u64, vp, vp]
+        L.orc_run_chunked.restype = i32
+        L.orc_run_chunked.argtypes = [i32, u64, u64, u64, i32, ctypes.POINTER(i32), u64, u64,
+                                      vp, i32, ctypes.POINTER(i32), ctypes.POINTER(i32), i32,
+                                      u64, vp, vp]
+        _lib = L
+    return _lib
+
+
+class OracleError(RuntimeError):
+    pass
+
+
+def _check(rc: int, what: str):
+    if rc != 0:
+        raise OracleError(f"oracle {what} failed with code {rc}")
+
+
+def _ptr(a: np.ndarray):
+    return ctypes.c_void_p(a.ctypes.data)
+
+
+def hash64(seed: int, stream: int, i: int) -> int:
+    return int(lib().orc_hash(seed, stream, i))
+
+
+def fill(etype: str, kind: str, count: int, *, seed: int = 42, stream: int = 0,
+         start: int = 0, n_rows: int = 1, k: int = 1) -> np.ndarray:
+    """Generate elements [start, start+count) of a (global) operand."""
+    out = np.empty(count, dtype=DTYPES[etype])
+    _check(lib().orc_fill(TYPES[etype], FILLS[kind], seed, stream, start, count, n_rows, k,
+                          _ptr(out)), "fill")
+    return out
+
+
+def _encode_program(program):
+    n = len(program)
+    ops = (ctypes.c_int * max(n, 1))(*[OPS[o] for o, _ in program])
+    args = (ctypes.c_int * max(n, 1))(*[int(a) for _, a in program])
+    return ops, args, n
+
+
+def _scalar_array(etype: str, scalars):
+    return np.array(list(scalars) if scalars else [0], dtype=DTYPES[etype])
+
+
+def eval_program(etype: str, program, operands, scalars=()) -> np.ndarray:
+    """Eager op-by-op evaluation: each node a new temporary."""
+    dt = DTYPES[etype]
+    ops_ = [np.ascontiguousarray(o, dtype=dt) for o in operands]
+    n = ops_[0].size if ops_ else 0
+    for o in ops_:
+        if o.size != n:
+            raise ValueError("operands must have the same number of elements")
+    ptrs = (ctypes.c_void_p * max(len(ops_), 1))(*[o.ctypes.data for o in ops_])
+    sc = _scalar_array(etype, scalars)
+    opc, argc, ni = _encode_program(program)
+    out = np.empty(n, dtype=dt)
+    _check(lib().orc_eval(TYPES[etype], n, ptrs, len(ops_), _ptr(sc), len(scalars), opc, argc,
+                          ni, _ptr(out)), "eval")
+    return out
+
+
+def reduce(etype: str, kind: str, v: np.ndarray):
+    """Full reduction; returns a numpy scalar of eT, or a 2-array for MINMAX."""
+    dt = DTYPES[etype]
+    v = np.ascontiguousarray(v, dtype=dt)
+    out = np.zeros(2, dtype=dt)
+    _check(lib().orc_reduce(TYPES[etype], KINDS[kind], v.size, _ptr(v), _ptr(out)), "reduce")
+    return out.copy() if kind == "MINMAX" else out[0]
+
+
+class Accumulator:
+    """Chunk-fed reduction state (bit-identical to a one-shot reduce)."""
+
+    def __init__(self, etype: str, kind: str):
+        self.etype, self.kind = etype, kind
+        self._buf = ctypes.create_string_buffer(int(lib().orc_acc_size()))
+        _check(lib().orc_acc_init(self._buf, TYPES[etype], KINDS[kind]), "acc_init")
+
+    def add(self, v: np.ndarray):
+        v = np.ascontiguousarray(v, dtype=DTYPES[self.etype])
+        _check(lib().orc_acc_add(self._buf, v.size, _ptr(v)), "acc_add")
+
+    def final(self):
+        out = np.zeros(2, dtype=DTYPES[self.etype])
+        _check(lib().orc_acc_final(self._buf, _ptr(out)), "acc_final")
+        return out.copy() if self.kind == "MINMAX" else out[0]
+
+
+def sum_dim(etype: str, dim: int, X: np.ndarray, n_rows: int, n_cols: int) -> np.ndarray:
+    """sum(X, dim) of a column-major n_rows x n_cols matrix stored as 1-D."""
+    dt = DTYPES[etype]
+    X = np.ascontiguousarray(X, dtype=dt).reshape(-1)
+    if X.size != n_rows * n_cols:
+        raise ValueError("X size mismatch")
+    out = np.empty(n_cols if dim == 0 else n_rows, dtype=dt)
+    _check(lib().orc_sum_dim(TYPES[etype], dim, n_rows, n_cols, _ptr(X), _ptr(out)), "sum_dim")
+    return out
+
+
+def run_chunked(etype: str, program, fills, *, start: int, count: int, n_rows: int = 1,
+                seed: int = 42, modk: int = 1, scalars=(), kind: str | None = None,
+                want_out: bool = False, chunk: int = 1 << 24):
+    """Evaluate `program` over global indices [start, start+count) with operands
+    regenerated per chunk (operand k uses stream k and fill kind fills[k]).
+    Returns (reduction result or None, element-wise result or None)."""
+    dt = DTYPES[etype]
+    fk = (ctypes.c_int * max(len(fills), 1))(*[FILLS[f] for f in fills])
+    sc = _scalar_array(etype, scalars)
+    opc, argc, ni = _encode_program(program)
+    acc = Accumulator(etype, kind) if kind else None
+    out = np.empty(count, dtype=dt) if want_out else None
+    _check(lib().orc_run_chunked(TYPES[etype], start, count, n_rows, len(fills), fk, seed, modk,
+                                 _ptr(sc), len(scalars), opc, argc, ni, chunk,
+                                 acc._buf if acc else None,
+                                 _ptr(out) if out is not None else None), "run_chunked")
+    return (acc.final() if acc else None), out

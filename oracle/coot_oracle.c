@@ -1,0 +1,575 @@
+/*
+ * ORACLE — TEST INFRASTRUCTURE ONLY.
+ *
+ * A plain, slow, obviously-correct CPU implementation of what the fused
+ * element-wise expression + reduction path computes.  Only tests/,
+ * __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference legs
+ * may load this library.  It shares no code, header, table or constant
+ * generator with the CUDA path under paper_2508_11385_b200/csrc/.
+ *
+ * What it follows (PAPER.md = /root/reference/PAPER.md):
+ *  - Eager evaluation (§3, "standard eager evaluation"): every
+ *    node of the expression produces a full temporary array, computed element
+ *    by element in the element type eT.  The delayed/fused GPU path must reach
+ *    the same values (reading R5: every node rounded to eT).
+ *  - eOp (element-wise unary incl. "multiplying matrix by scalar") and
+ *    eGlue (element-wise binary on objects of the same dimensions).
+ *  - `sum` of all elements (P:168 `float result = sum(A)`, P:517 task 1):
+ *    the exact sum, rounded once to eT (reading R10).  Accumulated with
+ *    long-double Neumaier compensation in index order, final add in
+ *    __float128 then one rounding to eT.
+ *  - sum(X,0) / sum(X,1): Armadillo convention (API compatibility P:144-152;
+ *    reading R3): dim 0 -> column sums (1 x n_cols), dim 1 -> row sums
+ *    (n_rows x 1); column-major storage (reading R2).
+ *  - min / max / norm2 / dot: readings R11-R13 in DESIGN.md.
+ *  - Input generator: SplitMix64 finaliser over (seed, stream, index)
+ *    (DESIGN.md "Input recipe"); fill::randu is uniform [0,1).
+ *
+ * Build: gcc -O2 -ffp-contract=off -fno-fast-math -fPIC -shared (x86-64 SSE2,
+ * FLT_EVAL_METHOD == 0) -lquadmath -lm.  See oracle/build.py.
+ */
+#include <math.h>
+#include <quadmath.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+/* ---- element types and opcodes (the oracle's own numbering) ------------ */
+enum { ORC_F32 = 0, ORC_F64 = 1, ORC_U32 = 2, ORC_S64 = 3 };
+
+enum {
+  ORC_LOAD = 0, ORC_SCALAR = 1,
+  ORC_NEG = 2, ORC_ABS = 3, ORC_SQUARE = 4, ORC_SQRT = 5, ORC_EXP = 6, ORC_LOG = 7,
+  ORC_ADD = 8, ORC_SUB = 9, ORC_MUL = 10, ORC_DIV = 11, ORC_MIN = 12, ORC_MAX = 13
+};
+
+enum { ORC_ACCU = 0, ORC_RMIN = 1, ORC_RMAX = 2, ORC_MINMAX = 3, ORC_NORM2 = 4 };
+
+enum {
+  ORC_E_OK = 0, ORC_E_TYPE = -1, ORC_E_PROGRAM = -2, ORC_E_NOMEM = -3,
+  ORC_E_EMPTY = -4, ORC_E_KIND = -5
+};
+
+static size_t esize(int type) {
+  switch (type) {
+    case ORC_F32: return 4;
+    case ORC_F64: return 8;
+    case ORC_U32: return 4;
+    case ORC_S64: return 8;
+  }
+  return 0;
+}
+
+/* ---- input generator ----------------------------------------------------
+ * mix(z): SplitMix64 finaliser (Vigna, splitmix64.c).
+ * key = seed ^ (stream * 0xD1B54A32D192ED03)
+ * h(i) = mix(key + (i+1) * 0x9E3779B97F4A7C15)   (wrapping uint64)
+ * With seed = stream = 0, h(0), h(1), ... is Vigna's splitmix64 sequence from
+ * state 0 (pinned in tests/golden/splitmix64_vigna.txt). */
+static uint64_t mix64(uint64_t z) {
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+
+uint64_t orc_hash(uint64_t seed, uint64_t stream, uint64_t i) {
+  uint64_t key = seed ^ (stream * 0xD1B54A32D192ED03ULL);
+  return mix64(key + (i + 1) * 0x9E3779B97F4A7C15ULL);
+}
+
+/* Fill kinds (structured variants for closed forms, DESIGN.md input recipe) */
+enum { ORC_FILL_RANDU = 0, ORC_FILL_ONES = 1, ORC_FILL_IOTA = 2, ORC_FILL_MODK = 3,
+       ORC_FILL_COLIDX = 4, ORC_FILL_ROWIDX = 5, ORC_FILL_ZEROS = 6 };
+
+/* Element g (global linear index) of a matrix with n_rows rows.  */
+static void fill_one(int type, int kind, uint64_t seed, uint64_t stream,
+                     uint64_t g, uint64_t n_rows, uint64_t k, void* out, uint64_t idx) {
+  uint64_t h = 0, iv = 0;
+  switch (kind) {
+    case ORC_FILL_RANDU: h = orc_hash(seed, stream, g); break;
+    case ORC_FILL_ONES: iv = 1; break;
+    case ORC_FILL_IOTA: iv = g; break;
+    case ORC_FILL_MODK: iv = g % k; break;
+    case ORC_FILL_COLIDX: iv = g / n_rows; break;
+    case ORC_FILL_ROWIDX: iv = g % n_rows; break;
+    case ORC_FILL_ZEROS: iv = 0; break;
+  }
+  if (kind == ORC_FILL_RANDU) {
+    switch (type) {
+      case ORC_F32: ((float*)out)[idx] = (float)(h >> 40) * 0x1p-24f; break;
+      case ORC_F64: ((double*)out)[idx] = (double)(h >> 11) * 0x1p-53; break;
+      case ORC_U32: ((uint32_t*)out)[idx] = (uint32_t)(h >> 32); break;
+      case ORC_S64: ((int64_t*)out)[idx] = (int64_t)h; break;
+    }
+  } else {
+    switch (type) {
+      case ORC_F32: ((float*)out)[idx] = (float)iv; break;
+      case ORC_F64: ((double*)out)[idx] = (double)iv; break;
+      case ORC_U32: ((uint32_t*)out)[idx] = (uint32_t)iv; break;
+      case ORC_S64: ((int64_t*)out)[idx] = (int64_t)iv; break;
+    }
+  }
+}
+
+int orc_fill(int type, int kind, uint64_t seed, uint64_t stream, uint64_t start,
+             uint64_t count, uint64_t n_rows, uint64_t k, void* out) {
+  if (esize(type) == 0) return ORC_E_TYPE;
+  if (n_rows == 0) n_rows = 1;
+  if (k == 0) k = 1;
+  for (uint64_t i = 0; i < count; ++i)
+    fill_one(type, kind, seed, stream, start + i, n_rows, k, out, i);
+  return ORC_E_OK;
+}
+
+/* ---- per-element semantics (readings R5-R9) -------------------
+ * Floating point: IEEE-754 binary32/binary64 round-to-nearest-even, each op
+ * computed in eT (compiled with -ffp-contract=off; SSE2, no x87 excess
+ * precision).  EXP/LOG are correctly rounded:
+ *   f32 exp: (float)exp((double)x)      f32 log: (float)logl((long double)x)
+ *   f64 exp: (double)expq((__float128)x) f64 log: (double)logq((__float128)x)
+ * (pinned against mpmath in tests/test_oracle_elementwise.py).
+ * MIN(a,b) = (b < a) ? b : a ; MAX(a,b) = (a < b) ? b : a   (reading R13).
+ * u32: arithmetic mod 2^32.  s64: two's complement mod 2^64, computed in
+ * uint64_t (reading R8).  Integer DIV/SQRT/EXP/LOG are rejected (R9). */
+
+static float f32_un(int op, float a) {
+  switch (op) {
+    case ORC_NEG: return -a;
+    case ORC_ABS: return fabsf(a);
+    case ORC_SQUARE: return a * a;
+    case ORC_SQRT: return sqrtf(a);
+    case ORC_EXP: return (float)exp((double)a);
+    case ORC_LOG: return (float)logl((long double)a);
+  }
+  return 0.0f;
+}
+
+static double f64_un(int op, double a) {
+  switch (op) {
+    case ORC_NEG: return -a;
+    case ORC_ABS: return fabs(a);
+    case ORC_SQUARE: return a * a;
+    case ORC_SQRT: return sqrt(a);
+    case ORC_EXP: return (double)expq((__float128)a);
+    case ORC_LOG: return (double)logq((__float128)a);
+  }
+  return 0.0;
+}
+
+static uint32_t u32_un(int op, uint32_t a) {
+  switch (op) {
+    case ORC_NEG: return (uint32_t)(0u - a);
+    case ORC_ABS: return a;
+    case ORC_SQUARE: return (uint32_t)(a * a);
+  }
+  return 0;
+}
+
+static uint64_t s64_un(int op, uint64_t a) {
+  switch (op) {
+    case ORC_NEG: return 0ULL - a;
+    case ORC_ABS: return ((int64_t)a < 0) ? 0ULL - a : a;
+    case ORC_SQUARE: return a * a;
+  }
+  return 0;
+}
+
+static float f32_bin(int op, float a, float b) {
+  switch (op) {
+    case ORC_ADD: return a + b;
+    case ORC_SUB: return a - b;
+    case ORC_MUL: return a * b;
+    case ORC_DIV: return a / b;
+    case ORC_MIN: return (b < a) ? b : a;
+    case ORC_MAX: return (a < b) ? b : a;
+  }
+  return 0.0f;
+}
+
+static double f64_bin(int op, double a, double b) {
+  switch (op) {
+    case ORC_ADD: return a + b;
+    case ORC_SUB: return a - b;
+    case ORC_MUL: return a * b;
+    case ORC_DIV: return a / b;
+    case ORC_MIN: return (b < a) ? b : a;
+    case ORC_MAX: return (a < b) ? b : a;
+  }
+  return 0.0;
+}
+
+static uint32_t u32_bin(int op, uint32_t a, uint32_t b) {
+  switch (op) {
+    case ORC_ADD: return (uint32_t)(a + b);
+    case ORC_SUB: return (uint32_t)(a - b);
+    case ORC_MUL: return (uint32_t)(a * b);
+    case ORC_MIN: return (b < a) ? b : a;
+    case ORC_MAX: return (a < b) ? b : a;
+  }
+  return 0;
+}
+
+static uint64_t s64_bin(int op, uint64_t a, uint64_t b) {
+  switch (op) {
+    case ORC_ADD: return a + b;
+    case ORC_SUB: return a - b;
+    case ORC_MUL: return a * b;
+    case ORC_MIN: return ((int64_t)b < (int64_t)a) ? b : a;
+    case ORC_MAX: return ((int64_t)a < (int64_t)b) ? b : a;
+  }
+  return 0;
+}
+
+static int is_unary(int op) { return op >= ORC_NEG && op <= ORC_LOG; }
+static int is_binary(int op) { return op >= ORC_ADD && op <= ORC_MAX; }
+static int legal_for(int type, int op) {
+  if (type == ORC_U32 || type == ORC_S64)
+    return !(op == ORC_SQRT || op == ORC_EXP || op == ORC_LOG || op == ORC_DIV);
+  return 1;
+}
+
+/* Unary op over a whole temporary: dst[i] = f(a[i]). */
+static void apply_unary(int type, int op, uint64_t n, const void* a, void* dst) {
+  for (uint64_t i = 0; i < n; ++i) {
+    switch (type) {
+      case ORC_F32: ((float*)dst)[i] = f32_un(op, ((const float*)a)[i]); break;
+      case ORC_F64: ((double*)dst)[i] = f64_un(op, ((const double*)a)[i]); break;
+      case ORC_U32: ((uint32_t*)dst)[i] = u32_un(op, ((const uint32_t*)a)[i]); break;
+      case ORC_S64: ((uint64_t*)dst)[i] = s64_un(op, ((const uint64_t*)a)[i]); break;
+    }
+  }
+}
+
+/* Binary op over whole temporaries: dst[i] = f(a[i], b[i]). */
+static void apply_binary(int type, int op, uint64_t n, const void* a, const void* b, void* dst) {
+  for (uint64_t i = 0; i < n; ++i) {
+    switch (type) {
+      case ORC_F32:
+        ((float*)dst)[i] = f32_bin(op, ((const float*)a)[i], ((const float*)b)[i]);
+        break;
+      case ORC_F64:
+        ((double*)dst)[i] = f64_bin(op, ((const double*)a)[i], ((const double*)b)[i]);
+        break;
+      case ORC_U32:
+        ((uint32_t*)dst)[i] = u32_bin(op, ((const uint32_t*)a)[i], ((const uint32_t*)b)[i]);
+        break;
+      case ORC_S64:
+        ((uint64_t*)dst)[i] = s64_bin(op, ((const uint64_t*)a)[i], ((const uint64_t*)b)[i]);
+        break;
+    }
+  }
+}
+
+/* ---- eager evaluation of a postfix program ------------------------------
+ * Postfix semantics: LOAD k pushes operand k; SCALAR k pushes scalar k
+ * (broadcast, materialised as a full temporary); a unary op pops a and pushes
+ * f(a); a binary op pops b (top) then a and pushes a OP b.  Every step
+ * allocates a NEW full temporary (the eager evaluation of P:366-367).  The
+ * program must leave exactly one entry, which is copied to `out`.
+ * `scalars` is an array of n_scalars values of eT. */
+#define ORC_MAX_STACK 64
+
+int orc_eval(int type, uint64_t n, const void* const* operands, int n_operands,
+             const void* scalars, int n_scalars, const int* ops, const int* args,
+             int n_instr, void* out) {
+  size_t es = esize(type);
+  if (es == 0) return ORC_E_TYPE;
+  void* stack[ORC_MAX_STACK];
+  int sp = 0;
+  int rc = ORC_E_OK;
+  size_t bytes = (size_t)n * es;
+  size_t alloc = bytes ? bytes : 1;
+  for (int pc = 0; pc < n_instr; ++pc) {
+    int op = ops[pc], arg = args[pc];
+    if (!legal_for(type, op)) { rc = ORC_E_PROGRAM; goto fail; }
+    if (op == ORC_LOAD) {
+      if (arg < 0 || arg >= n_operands || sp >= ORC_MAX_STACK) { rc = ORC_E_PROGRAM; goto fail; }
+      void* t = malloc(alloc);
+      if (!t) { rc = ORC_E_NOMEM; goto fail; }
+      if (bytes) memcpy(t, operands[arg], bytes);
+      stack[sp++] = t;
+    } else if (op == ORC_SCALAR) {
+      if (arg < 0 || arg >= n_scalars || sp >= ORC_MAX_STACK) { rc = ORC_E_PROGRAM; goto fail; }
+      void* t = malloc(alloc);
+      if (!t) { rc = ORC_E_NOMEM; goto fail; }
+      for (uint64_t i = 0; i < n; ++i)
+        memcpy((char*)t + i * es, (const char*)scalars + (size_t)arg * es, es);
+      stack[sp++] = t;
+    } else if (is_unary(op)) {
+      if (sp < 1) { rc = ORC_E_PROGRAM; goto fail; }
+      void* t = malloc(alloc);
+      if (!t) { rc = ORC_E_NOMEM; goto fail; }
+      apply_unary(type, op, n, stack[sp - 1], t);
+      free(stack[sp - 1]);
+      stack[sp - 1] = t;
+    } else if (is_binary(op)) {
+      if (sp < 2) { rc = ORC_E_PROGRAM; goto fail; }
+      void* t = malloc(alloc);
+      if (!t) { rc = ORC_E_NOMEM; goto fail; }
+      apply_binary(type, op, n, stack[sp - 2], stack[sp - 1], t);
+      free(stack[sp - 1]);
+      free(stack[sp - 2]);
+      sp -= 2;
+      stack[sp++] = t;
+    } else {
+      rc = ORC_E_PROGRAM;
+      goto fail;
+    }
+  }
+  if (sp != 1) { rc = ORC_E_PROGRAM; goto fail; }
+  if (bytes) memcpy(out, stack[0], bytes);
+  free(stack[0]);
+  return ORC_E_OK;
+fail:
+  while (sp > 0) free(stack[--sp]);
+  return rc;
+}
+
+/* ---- reductions ---------------------------------------------------------
+ * Accumulator state so that a reduction can be fed chunk by chunk (the
+ * chunked mode is bit-identical to one call over the whole array: same
+ * operations in the same index order). */
+typedef struct {
+  int type, kind;
+  long double s, c;      /* Neumaier sum and compensation (floats)          */
+  uint64_t isum;         /* modular integer sum                              */
+  uint64_t count;
+  double fmin, fmax;     /* running min/max for floats (f32 values exact)   */
+  uint64_t umin, umax;   /* running min/max for ints (bits)                  */
+} orc_acc;
+
+size_t orc_acc_size(void) { return sizeof(orc_acc); }
+
+int orc_acc_init(orc_acc* a, int type, int kind) {
+  if (esize(type) == 0) return ORC_E_TYPE;
+  if (kind < ORC_ACCU || kind > ORC_NORM2) return ORC_E_KIND;
+  if (kind == ORC_NORM2 && (type == ORC_U32 || type == ORC_S64)) return ORC_E_KIND;
+  memset(a, 0, sizeof(*a));
+  a->type = type;
+  a->kind = kind;
+  return ORC_E_OK;
+}
+
+/* Neumaier (improved Kahan-Babuska) step in long double. */
+static void neumaier(long double* s, long double* c, long double x) {
+  long double t = *s + x;
+  if (fabsl(*s) >= fabsl(x))
+    *c += (*s - t) + x;
+  else
+    *c += (x - t) + *s;
+  *s = t;
+}
+
+static long double elem_as_ld(int type, const void* v, uint64_t i) {
+  if (type == ORC_F32) return (long double)((const float*)v)[i];
+  return (long double)((const double*)v)[i];
+}
+
+static uint64_t elem_as_u64(int type, const void* v, uint64_t i) {
+  if (type == ORC_U32) return (uint64_t)((const uint32_t*)v)[i];
+  return ((const uint64_t*)v)[i];
+}
+
+static int int_less(int type, uint64_t a, uint64_t b) {
+  if (type == ORC_S64) return (int64_t)a < (int64_t)b;
+  return a < b;
+}
+
+int orc_acc_add(orc_acc* a, uint64_t n, const void* v) {
+  int type = a->type;
+  for (uint64_t i = 0; i < n; ++i) {
+    if (type == ORC_F32 || type == ORC_F64) {
+      long double x = elem_as_ld(type, v, i);
+      switch (a->kind) {
+        case ORC_ACCU: neumaier(&a->s, &a->c, x); break;
+        case ORC_NORM2: neumaier(&a->s, &a->c, x * x); break;
+        default: {
+          double d = (double)x;
+          if (a->count == 0) { a->fmin = d; a->fmax = d; }
+          else {
+            if (d < a->fmin) a->fmin = d;
+            if (a->fmax < d) a->fmax = d;
+          }
+        }
+      }
+    } else {
+      uint64_t x = elem_as_u64(type, v, i);
+      if (a->kind == ORC_ACCU) {
+        a->isum += x;
+      } else {
+        if (a->count == 0) { a->umin = x; a->umax = x; }
+        else {
+          if (int_less(type, x, a->umin)) a->umin = x;
+          if (int_less(type, a->umax, x)) a->umax = x;
+        }
+      }
+    }
+    a->count++;
+  }
+  return ORC_E_OK;
+}
+
+/* Exact value of the Neumaier state rounded once: s + c is formed in
+ * __float128 (113-bit significand) and rounded to eT. */
+static __float128 acc_total(const orc_acc* a) {
+  return (__float128)a->s + (__float128)a->c;
+}
+
+/* result: 1 eT (ACCU/MIN/MAX/NORM2) or 2 eT (MINMAX: [min, max]). */
+int orc_acc_final(const orc_acc* a, void* result) {
+  int type = a->type;
+  if ((a->kind == ORC_RMIN || a->kind == ORC_RMAX || a->kind == ORC_MINMAX) && a->count == 0)
+    return ORC_E_EMPTY;
+  if (type == ORC_F32 || type == ORC_F64) {
+    double r0 = 0, r1 = 0;
+    int two = 0;
+    switch (a->kind) {
+      case ORC_ACCU:
+        if (type == ORC_F32) { ((float*)result)[0] = (float)acc_total(a); return ORC_E_OK; }
+        ((double*)result)[0] = (double)acc_total(a);
+        return ORC_E_OK;
+      case ORC_NORM2: {
+        __float128 r = sqrtq(acc_total(a));
+        if (type == ORC_F32) ((float*)result)[0] = (float)r;
+        else ((double*)result)[0] = (double)r;
+        return ORC_E_OK;
+      }
+      case ORC_RMIN: r0 = a->fmin; break;
+      case ORC_RMAX: r0 = a->fmax; break;
+      case ORC_MINMAX: r0 = a->fmin; r1 = a->fmax; two = 1; break;
+    }
+    if (type == ORC_F32) {
+      ((float*)result)[0] = (float)r0;
+      if (two) ((float*)result)[1] = (float)r1;
+    } else {
+      ((double*)result)[0] = r0;
+      if (two) ((double*)result)[1] = r1;
+    }
+    return ORC_E_OK;
+  }
+  uint64_t r0 = 0, r1 = 0;
+  int two = 0;
+  switch (a->kind) {
+    case ORC_ACCU: r0 = a->isum; break;
+    case ORC_RMIN: r0 = a->umin; break;
+    case ORC_RMAX: r0 = a->umax; break;
+    case ORC_MINMAX: r0 = a->umin; r1 = a->umax; two = 1; break;
+  }
+  if (type == ORC_U32) {
+    ((uint32_t*)result)[0] = (uint32_t)r0;
+    if (two) ((uint32_t*)result)[1] = (uint32_t)r1;
+  } else {
+    ((uint64_t*)result)[0] = r0;
+    if (two) ((uint64_t*)result)[1] = r1;
+  }
+  return ORC_E_OK;
+}
+
+/* One-shot full reduction of v[0..n). */
+int orc_reduce(int type, int kind, uint64_t n, const void* v, void* result) {
+  orc_acc a;
+  int rc = orc_acc_init(&a, type, kind);
+  if (rc) return rc;
+  orc_acc_add(&a, n, v);
+  return orc_acc_final(&a, result);
+}
+
+/* ---- dimension sums (reading R3) ----------------------------------------
+ * X is column-major m x n (element (i,j) at X[i + j*m]).
+ * dim 0: out[j] = sum_{i=0..m-1} X(i,j)   (n_cols results, a Row)
+ * dim 1: out[i] = sum_{j=0..n-1} X(i,j)   (n_rows results, a Col)
+ * Each output is its own exact-then-rounded sum (Neumaier over the stated
+ * index order).  For dim 1 the loop nest visits j outer / i inner so memory
+ * is read contiguously; every row's own summation order is still j = 0..n-1,
+ * so the arithmetic is exactly that of the plain per-row loop. */
+int orc_sum_dim(int type, int dim, uint64_t m, uint64_t n, const void* X, void* out) {
+  size_t es = esize(type);
+  if (es == 0) return ORC_E_TYPE;
+  int is_float = (type == ORC_F32 || type == ORC_F64);
+  if (dim == 0) {
+    for (uint64_t j = 0; j < n; ++j) {
+      orc_acc a;
+      orc_acc_init(&a, type, ORC_ACCU);
+      orc_acc_add(&a, m, (const char*)X + (size_t)(j * m) * es);
+      orc_acc_final(&a, (char*)out + (size_t)j * es);
+    }
+    return ORC_E_OK;
+  }
+  if (dim != 1) return ORC_E_KIND;
+  long double* s = NULL;
+  long double* c = NULL;
+  uint64_t* u = NULL;
+  size_t mm = m ? m : 1;
+  if (is_float) {
+    s = (long double*)calloc(mm, sizeof(long double));
+    c = (long double*)calloc(mm, sizeof(long double));
+    if (!s || !c) { free(s); free(c); return ORC_E_NOMEM; }
+  } else {
+    u = (uint64_t*)calloc(mm, sizeof(uint64_t));
+    if (!u) return ORC_E_NOMEM;
+  }
+  for (uint64_t j = 0; j < n; ++j) {
+    const char* col = (const char*)X + (size_t)(j * m) * es;
+    for (uint64_t i = 0; i < m; ++i) {
+      if (is_float) neumaier(&s[i], &c[i], elem_as_ld(type, col, i));
+      else u[i] += elem_as_u64(type, col, i);
+    }
+  }
+  for (uint64_t i = 0; i < m; ++i) {
+    switch (type) {
+      case ORC_F32: ((float*)out)[i] = (float)((__float128)s[i] + (__float128)c[i]); break;
+      case ORC_F64: ((double*)out)[i] = (double)((__float128)s[i] + (__float128)c[i]); break;
+      case ORC_U32: ((uint32_t*)out)[i] = (uint32_t)u[i]; break;
+      case ORC_S64: ((uint64_t*)out)[i] = u[i]; break;
+    }
+  }
+  free(s);
+  free(c);
+  free(u);
+  return ORC_E_OK;
+}
+
+/* ---- chunked mode --------------------------------------------------------
+ * Evaluate a program over global indices [start, start+count) whose operands
+ * are regenerated chunk by chunk from (seed, stream = operand index, global
+ * index) with per-operand fill kinds, feeding the reduction accumulator `acc`
+ * (may be NULL) and optionally writing the element-wise result to `out`
+ * (count elements, may be NULL).  Because every step is the same element-wise
+ * arithmetic and the accumulator consumes elements in index order, this is
+ * bit-identical to generating everything and calling orc_eval + orc_reduce
+ * once (tested).  Lets 2^32-element configurations fit in host RAM. */
+int orc_run_chunked(int type, uint64_t start, uint64_t count, uint64_t n_rows,
+                    int n_operands, const int* fill_kinds, uint64_t seed, uint64_t modk,
+                    const void* scalars, int n_scalars, const int* ops, const int* args,
+                    int n_instr, uint64_t chunk, orc_acc* acc, void* out) {
+  size_t es = esize(type);
+  if (es == 0) return ORC_E_TYPE;
+  if (n_operands < 0 || n_operands > 16) return ORC_E_PROGRAM;
+  if (chunk == 0) chunk = (uint64_t)1 << 24;
+  void* bufs[16];
+  const void* cops[16];
+  void* res = malloc((size_t)chunk * es);
+  if (!res) return ORC_E_NOMEM;
+  for (int k = 0; k < n_operands; ++k) {
+    bufs[k] = malloc((size_t)chunk * es);
+    if (!bufs[k]) {
+      for (int q = 0; q < k; ++q) free(bufs[q]);
+      free(res);
+      return ORC_E_NOMEM;
+    }
+    cops[k] = bufs[k];
+  }
+  int rc = ORC_E_OK;
+  for (uint64_t off = 0; off < count; off += chunk) {
+    uint64_t len = count - off < chunk ? count - off : chunk;
+    for (int k = 0; k < n_operands; ++k)
+      orc_fill(type, fill_kinds[k], seed, (uint64_t)k, start + off, len, n_rows, modk, bufs[k]);
+    rc = orc_eval(type, len, cops, n_operands, scalars, n_scalars, ops, args, n_instr, res);
+    if (rc) break;
+    if (acc) orc_acc_add(acc, len, res);
+    if (out) memcpy((char*)out + (size_t)off * es, res, (size_t)len * es);
+  }
+  for (int k = 0; k < n_operands; ++k) free(bufs[k]);
+  free(res);
+  return rc;
+}
