@@ -1,0 +1,397 @@
+#!/usr/bin/env python
+"""Benchmark of the fused element-wise expression + reduction path.
+
+Workload (BASELINE.json configs[1], the config `metric` is quoted on):
+    Z = exp(A % B) + 3*C ; accu(Z)      A, B, C: 10000 x 10000 f32, fill::randu
+One STEP = one pass of the whole hot path: expression capture (delayed
+evaluation) -> validate/lower -> ONE fused kernel that writes Z and reduces it
+-> (N > 1) exchange of the 32-byte partials over NCCL + rank-order combine
+kernel.  Weak scaling: every rank owns a 10000 x 10000 column block of a
+10000 x (10000 N) global matrix (generated on the device from the global
+element index, so the global data do not depend on N).
+
+Usage: python bench.py [--gpus N] [--steps K] [--warmup W] [--impl coot|reference]
+Under torchrun (N > 1) every rank runs; rank 0 prints ONE JSON line.
+`--impl reference` times the CPU oracle (oracle/, the reference arm of this
+tier) on the same workload, a bounded sample per step.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+M_ROWS, N_COLS = 10_000, 10_000
+PROGRAM = [("LOAD", 0), ("LOAD", 1), ("MUL", 0), ("EXP", 0), ("SCALAR", 0), ("LOAD", 2),
+           ("MUL", 0), ("ADD", 0)]
+SCALARS = [3.0]
+BYTES_PER_ELEM = 16  # 3 f32 reads + 1 f32 write (Z stored), SURVEY §8(d) / DESIGN.md
+METRIC = "fused-expression GB/s and elements/s vs HBM peak at 1/2/4/8 B200; vs CPU oracle"
+WORKLOAD = ("c2: Z = exp(A % B) + 3*C then accu(Z), 10000x10000 f32 Mat per GPU "
+            "(BASELINE.json configs[1])")
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def _traffic():
+    """dram read+write bytes per launch of the fused kernel from the committed
+    ncu --set full capture (profiles/), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            t = json.load(f)
+        return t.get("c2_eval_accu", {}).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled while the GPU is under load."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, uuids):
+        self.uuids = uuids
+        self.proc = None
+        self.path = f"/tmp/coot_clocks_{os.getpid()}.csv"
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={','.join(self.uuids)}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        rows = []
+        for line in open(self.path):
+            f = [x.strip() for x in line.split(",")]
+            if len(f) >= 8:
+                rows.append(f)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+
+        def num(x):
+            try:
+                return float(x)
+            except ValueError:
+                return None
+        sm = [num(r[0]) for r in rows if num(r[0])]
+        pw = [num(r[2]) for r in rows if num(r[2])]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[4 + i] == "Active"})
+        # under-load samples: the upper half of observed power
+        if pw:
+            cut = sorted(pw)[len(pw) // 2]
+            sm_load = [num(r[0]) for r in rows if num(r[2]) and num(r[2]) >= cut and num(r[0])]
+        else:
+            sm_load = sm
+        sm_load = sorted(sm_load or sm)
+        return {"sm_mhz": sm_load[len(sm_load) // 2], "sm_max_mhz": num(rows[0][1]),
+                "reasons": reasons, "samples": len(rows),
+                "power_w_max": max(pw) if pw else None}
+
+
+def run_reference(args):
+    """Reference arm: the CPU oracle, as it stands, on the same workload."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import numpy as np
+
+    import oracle
+    total = args.steps + args.warmup
+    # calibrate ns/element of the oracle on this host, then size each step so the
+    # whole --steps/--warmup run stays within ~90 s of CPU work
+    cal_n = 1 << 20
+    cal = [oracle.fill("f32", "randu", cal_n, stream=s) for s in range(3)]
+    t0 = time.perf_counter()
+    z = oracle.eval_program("f32", PROGRAM, cal, SCALARS)
+    oracle.reduce("f32", "ACCU", z)
+    ns_per_el = (time.perf_counter() - t0) / cal_n * 1e9
+    budget_s = float(os.environ.get("COOT_REF_BUDGET_S", "90"))
+    per_step = int(min(M_ROWS * N_COLS, max(1 << 16, budget_s / total / (ns_per_el * 1e-9))))
+    per_step = per_step // M_ROWS * M_ROWS or M_ROWS  # whole columns of the matrix
+    ops = [oracle.fill("f32", "randu", per_step, stream=s) for s in range(3)]
+    times = []
+    for i in range(total):
+        t0 = time.perf_counter()
+        z = oracle.eval_program("f32", PROGRAM, ops, SCALARS)
+        r = oracle.reduce("f32", "ACCU", z)
+        dt = time.perf_counter() - t0
+        if i >= args.warmup:
+            times.append(dt)
+    t = sum(times) / len(times)
+    gbs = per_step * BYTES_PER_ELEM / t / 1e9
+    sample = (f"first {per_step // M_ROWS} of 10000 columns ({per_step} elements) of the c2 "
+              f"workload per step, single-threaded oracle, generation untimed")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": gbs, "unit": "GB/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "n_rows": M_ROWS, "n_cols": N_COLS,
+                   "mode": "eval+accu (Z stored)"},
+        "elements_per_s": per_step / t,
+        "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": 1, "kind": "oracle",
+                         "sample": sample},
+        "e2e": {"value": gbs, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "result_sample": float(r),
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def cpu_baseline_oracle():
+    """The oracle timed on this host on the full c2 workload (1e8 elements),
+    single-threaded; input generation untimed.  Returns (record, accu)."""
+    import oracle
+    n = M_ROWS * N_COLS
+    ops = [oracle.fill("f32", "randu", n, stream=s) for s in range(3)]
+    t0 = time.perf_counter()
+    z = oracle.eval_program("f32", PROGRAM, ops, SCALARS)
+    r = oracle.reduce("f32", "ACCU", z)
+    dt = time.perf_counter() - t0
+    del ops, z
+    gbs = n * BYTES_PER_ELEM / dt / 1e9
+    rec = {"value": gbs, "unit": "GB/s", "cores": 1, "kind": "oracle",
+           "sample": f"full c2 workload on rank 0's block ({n} elements), one pass, "
+                     f"{dt:.2f} s single-threaded, generation untimed",
+           "elements_per_s": n / dt}
+    return rec, float(r)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="coot", choices=["coot", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    import paper_2508_11385_b200 as coot
+    from paper_2508_11385_b200 import dist as cdist
+
+    stream = torch.cuda.current_stream()
+    ctx = coot.Context(local, stream=stream)
+    n = M_ROWS * N_COLS
+    start = rank * n  # global element index of this rank's column block
+    dev = torch.device("cuda", local)
+    data = [torch.empty(n, dtype=torch.float32, device=dev) for _ in range(3)]
+    for s, t in enumerate(data):
+        ctx.fill(t, "randu", seed=42, stream=s, start=start, n_rows=M_ROWS)
+    A, B, C = (coot.Mat(t, M_ROWS, N_COLS) for t in data)
+    Z = coot.Mat.empty(M_ROWS, N_COLS, "f32", device=dev)
+    reducer = cdist.DistReducer(ctx) if world > 1 else None
+
+    kern_ev = []
+
+    def step(record=False):
+        # a1: expression capture (delayed evaluation); a2-a4: one fused launch
+        e = coot.exp(A % B) + 3 * C
+        lw = coot.lower(e)
+        if record:
+            e0 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+        if reducer is None:
+            res = torch.empty(1, dtype=torch.float32, device=dev)
+            ctx.reduce(lw.elem, lw.n_rows, lw.n_cols, lw.program, lw.operands, lw.scalars,
+                       "ACCU", res, Z.data)
+            if record:
+                e1 = torch.cuda.Event(enable_timing=True)
+                e1.record(stream)
+                kern_ev.append((e0, e1))
+            return res
+        # a6: partial -> NCCL all-gather -> rank-order combine kernel
+        res = reducer.reduce(lw, "ACCU", out=Z.data,
+                             kernel_events=kern_ev if record else None)
+        return res
+
+    peak, peak_kind = _peaks()
+    uuids = []
+    try:
+        uuids = [str(torch.cuda.get_device_properties(local).uuid)]
+        uuids = [u if u.startswith("GPU-") else "GPU-" + u for u in uuids]
+    except Exception:
+        pass
+    sampler = ClockSampler(uuids) if rank == 0 else None
+    if sampler:
+        sampler.start()
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = ctx.stats()["launches"]
+    t_begin = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    t_begin.record(stream)
+    last = None
+    for _ in range(args.steps):
+        last = step(record=True)
+    t_end.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = sampler.stop() if sampler else None
+    launches = ctx.stats()["launches"] - launches0
+    elapsed_ms = t_begin.elapsed_time(t_end)
+    kern_ms = sum(a.elapsed_time(b) for a, b in kern_ev) / max(1, len(kern_ev))
+    if world > 1:
+        tt = torch.tensor([elapsed_ms, kern_ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        elapsed_ms, kern_ms = float(tt[0]), float(tt[1])
+    ms_per_step = elapsed_ms / args.steps
+    total_elems = n * world
+    value = total_elems * BYTES_PER_ELEM / (ms_per_step * 1e-3) / 1e9
+    accu = float(last.item())
+
+    # reduce-only variant (12 B/el), informational
+    torch.cuda.synchronize()
+    ro_res = torch.empty(1, dtype=torch.float32, device=dev)
+    lw = coot.lower(coot.exp(A % B) + 3 * C)
+    for _ in range(3):
+        ctx.reduce(lw.elem, lw.n_rows, lw.n_cols, lw.program, lw.operands, lw.scalars, "ACCU",
+                   ro_res)
+    r0 = torch.cuda.Event(enable_timing=True)
+    r1 = torch.cuda.Event(enable_timing=True)
+    r0.record(stream)
+    nro = 50
+    for _ in range(nro):
+        ctx.reduce(lw.elem, lw.n_rows, lw.n_cols, lw.program, lw.operands, lw.scalars, "ACCU",
+                   ro_res)
+    r1.record(stream)
+    torch.cuda.synchronize()
+    ro_ms = r0.elapsed_time(r1) / nro
+
+    # e2e: the same step through the public API with HOST inputs (pinned) — the
+    # H2D copies of A, B, C and the D2H read of accu are inside the timed region
+    e2e = None
+    if args.e2e_steps > 0:
+        host = [t.cpu().pin_memory() for t in data]
+        r_host = torch.empty(1, dtype=torch.float32).pin_memory()
+        torch.cuda.synchronize()
+
+        def e2e_step():
+            for h, d in zip(host, data):
+                d.copy_(h, non_blocking=True)
+            r = step()
+            r_host.copy_(r[:1], non_blocking=True)
+
+        e2e_step()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        x0 = torch.cuda.Event(enable_timing=True)
+        x1 = torch.cuda.Event(enable_timing=True)
+        x0.record(stream)
+        for _ in range(args.e2e_steps):
+            e2e_step()
+        x1.record(stream)
+        torch.cuda.synchronize()
+        e_ms = x0.elapsed_time(x1) / args.e2e_steps
+        if world > 1:
+            tt = torch.tensor([e_ms], dtype=torch.float64, device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            e_ms = float(tt[0])
+        e2e = {"value": total_elems * BYTES_PER_ELEM / (e_ms * 1e-3) / 1e9, "unit": "GB/s",
+               "h2d_bytes_per_step": 3 * n * 4, "d2h_bytes_per_step": 4,
+               "ms_per_step": e_ms}
+        del host
+
+    if rank != 0:
+        if world > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return 0
+
+    cpu = None
+    parity = None
+    if world == 1 and not args.no_cpu_baseline:
+        cpu, ref_accu = cpu_baseline_oracle()
+        parity = {"accu": accu, "oracle_accu": ref_accu,
+                  "rel_err": abs(accu - ref_accu) / abs(ref_accu)}
+
+    alg_bytes = n * BYTES_PER_ELEM
+    achieved = alg_bytes / (kern_ms * 1e-3) / 1e9
+    line = {
+        "metric": METRIC,
+        "value": value,
+        "unit": "GB/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms_per_step,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f32",
+        "data": "synthetic",
+        "config": {"workload": WORKLOAD, "n_rows": M_ROWS, "n_cols": N_COLS,
+                   "global_elements": total_elems, "mode": "eval+accu (Z stored)",
+                   "parallelism": f"dp{world} (column blocks)",
+                   "l2": "inputs 1.2 GB + output 0.4 GB per GPU >> 126 MB L2; no flush needed"},
+        "elements_per_s": total_elems / (ms_per_step * 1e-3),
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": _traffic(),
+                     "peak_kind": peak_kind,
+                     "kernel": "fused_kernel<float, ACC_SUM, catalog 2> (c2 program)",
+                     "alg_bytes_per_launch": alg_bytes, "kernel_ms": kern_ms},
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": launches,
+        "clocks": clocks,
+        "variants": {"reduce_only_GBps": n * 12 / (ro_ms * 1e-3) / 1e9,
+                     "reduce_only_ms": ro_ms},
+        "parity": parity,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,220 @@
+/*
+ * coot.h — C ABI of libcoot: a B200-native (sm_100a) fused element-wise
+ * expression + reduction engine, written from the problem statement of
+ * "Bandicoot: A Templated C++ Library for GPU Linear Algebra"
+ * (Curtin, Edel, Sanderson; arXiv 2508.11385).  P:n = line n of the paper
+ * source; R<k> = reading k in DESIGN.md.
+ *
+ * What the calls compute
+ *   An expression assigned to a matrix is evaluated only at assignment
+ *   ("delayed evaluation", §3) and the whole expression is mapped
+ *   to "the minimal set of calls"; here that is ONE kernel launch
+ *   per coot_eval / coot_reduce on one GPU.  The expression is an eOp/eGlue
+ *   tree (element-wise unary incl. scalar multiply; element-wise
+ *   binary on same-dimension operands) encoded as a postfix program.
+ *   Optional terminal reductions: accu / sum of all elements,
+ *   min, max, norm2, and sum(X,0) / sum(X,1) (Armadillo convention, R3).
+ *   Element types f32, f64 (fmat/dmat), u32, s64.
+ *
+ * Conventions (every call)
+ *   - All data pointers (operands, out, result, partials) are CUDA device
+ *     pointers on the ctx's device.  Matrices are dense column-major with
+ *     leading dimension n_rows (R2); Col = n x 1, Row = 1 x n.
+ *   - The caller owns every data buffer; libcoot never allocates user-visible
+ *     memory.  A ctx owns its scratch (reduction records, tickets), allocated
+ *     in coot_init / grown on first need, freed in coot_destroy.
+ *   - Work is enqueued on the ctx stream; results are valid after that stream
+ *     is synchronised (results live in device memory: a host read is an
+ *     explicit copy).  Validation errors are returned synchronously
+ *     BEFORE anything is enqueued (no partial side effects).  Asynchronous
+ *     device faults surface at coot_sync.
+ *   - The descriptor is read only during the call and may be reused after.
+ *   - A ctx is not thread-safe; use one ctx per (thread, stream).
+ *   - Every non-OK status sets a thread-local message naming the category and
+ *     the specifics (coot_last_error), e.g. "conformability: operand 2 is
+ *     100x99, expression is 100x100 (LOAD @ instr 5)".
+ */
+#ifndef COOT_H
+#define COOT_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define COOT_ABI_VERSION 1u
+#define COOT_MAX_OPERANDS 8 /* operand arrays per expression */
+#define COOT_MAX_SCALARS 8  /* scalar slots per expression   */
+#define COOT_MAX_INSTR 32   /* postfix instructions          */
+#define COOT_MAX_STACK 8    /* evaluation stack depth        */
+#define COOT_PARTIAL_BYTES 32u /* one scalar reduction partial record */
+
+typedef enum { COOT_F32 = 0, COOT_F64 = 1, COOT_U32 = 2, COOT_S64 = 3 } coot_elem_t;
+
+typedef enum {
+  COOT_OK = 0,
+  COOT_ERR_CONFIG = 1,   /* bad device / ctx / stream, compute capability != 10.x   */
+  COOT_ERR_CONFORM = 2,  /* operand dims disagree with the expression       */
+  COOT_ERR_BOUNDS = 3,   /* more than the operand/scalar/instr/stack limits above   */
+  COOT_ERR_RESOURCE = 4, /* scratch allocation failed                               */
+  COOT_ERR_CONTRACT = 5, /* malformed program, op illegal for the type (R9),
+                            NORM2 on integers, bad alias, min/max of empty,
+                            null pointer with n > 0, unsupported layout          */
+  COOT_ERR_DEVICE = 6    /* CUDA error (message via coot_last_error)              */
+} coot_status;
+
+/* Postfix opcodes.  LOAD k pushes operand k; SCALAR k pushes scalar k;
+ * unary ops pop a, push f(a); binary ops pop b (top) then a, push a OP b.
+ * Every node is rounded to the element type; no FMA contraction (R5).
+ * MUL is both the Schur product '%' (R1) and scalar multiply.
+ * MIN(a,b) = (b < a) ? b : a ; MAX(a,b) = (a < b) ? b : a (R13).
+ * u32 wraps mod 2^32, s64 is two's complement mod 2^64 (R8).
+ * SQRT, EXP, LOG, DIV are f32/f64 only (R9). */
+typedef enum {
+  COOT_OP_LOAD = 0, COOT_OP_SCALAR = 1,
+  COOT_OP_NEG = 2, COOT_OP_ABS = 3, COOT_OP_SQUARE = 4,
+  COOT_OP_SQRT = 5, COOT_OP_EXP = 6, COOT_OP_LOG = 7,
+  COOT_OP_ADD = 8, COOT_OP_SUB = 9, COOT_OP_MUL = 10, COOT_OP_DIV = 11,
+  COOT_OP_MIN = 12, COOT_OP_MAX = 13,
+  COOT_OP_COUNT_ = 14
+} coot_opcode;
+
+typedef struct {
+  uint8_t op;  /* coot_opcode                      */
+  uint8_t arg; /* operand / scalar index, else 0   */
+} coot_instr;
+
+/* A scalar operand, stored AS the element type (R4): the value 2.5 of an f32
+ * expression is {.f32 = 2.5f}. */
+typedef union {
+  float f32;
+  double f64;
+  uint32_t u32;
+  int64_t s64;
+  uint64_t bits;
+} coot_scalar;
+
+/* One dense operand.  n_rows/n_cols must equal the expression's (eGlue
+ * "same dimensions") else COOT_ERR_CONFORM.  ld = leading dimension in
+ * elements; 0 means n_rows.  ABI v1 requires ld == n_rows (contiguous). */
+typedef struct {
+  const void* ptr;
+  uint64_t n_rows, n_cols;
+  uint64_t ld;
+} coot_operand;
+
+/* The expression descriptor: the runtime encoding of the compound expression
+ * type — pointers plus "a few integers of metadata". */
+typedef struct {
+  uint32_t abi_version; /* = COOT_ABI_VERSION                           */
+  uint32_t elem;        /* coot_elem_t                                  */
+  uint64_t n_rows, n_cols; /* dims of the element-wise result          */
+  uint32_t n_operands;  /* 1..COOT_MAX_OPERANDS                         */
+  uint32_t n_scalars;   /* 0..COOT_MAX_SCALARS                          */
+  uint32_t n_instr;     /* 1..COOT_MAX_INSTR                            */
+  uint32_t reserved;    /* must be 0                                    */
+  coot_operand operands[COOT_MAX_OPERANDS];
+  coot_scalar scalars[COOT_MAX_SCALARS];
+  coot_instr prog[COOT_MAX_INSTR];
+} coot_expr;
+
+/* Terminal reductions and the shape of `result`:
+ *   ACCU, MIN, MAX, NORM2 -> 1 eT;  MINMAX -> 2 eT [min, max];
+ *   SUM_DIM0 -> n_cols eT (a Row of column sums);
+ *   SUM_DIM1 -> n_rows eT (a Col of row sums).
+ * ACCU of floats accumulates in f64 and rounds once to eT (R10); integer
+ * ACCU is modular.  NORM2 = sqrt(sum v^2), floats only (R12).
+ * MIN/MAX/MINMAX of an empty expression -> COOT_ERR_CONTRACT; ACCU, NORM2 of
+ * empty -> 0; SUM_DIM over a zero-length dimension -> zeros. */
+typedef enum {
+  COOT_RED_ACCU = 0, COOT_RED_MIN = 1, COOT_RED_MAX = 2, COOT_RED_MINMAX = 3,
+  COOT_RED_NORM2 = 4, COOT_RED_SUM_DIM0 = 5, COOT_RED_SUM_DIM1 = 6,
+  COOT_RED_COUNT_ = 7
+} coot_reduce_kind;
+
+typedef struct coot_ctx coot_ctx;
+
+#define COOT_INIT_PRINT_INFO 1u   /* print device info to stderr */
+#define COOT_INIT_FORCE_INTERP 2u /* always use the interpreter kernel (tests)  */
+
+/* Bind a ctx to CUDA `device` and `cuda_stream` (a cudaStream_t; NULL = the
+ * legacy default stream).  Requires compute capability 10.x (sm_100a build).
+ * The analogue of coot_init("cuda", print_info, device) minus
+ * backend selection (CUDA only).  *out receives the ctx. */
+coot_status coot_init(coot_ctx** out, int device, void* cuda_stream, uint32_t flags);
+coot_status coot_destroy(coot_ctx* ctx);
+coot_status coot_set_stream(coot_ctx* ctx, void* cuda_stream);
+
+/* Host-only checks (no CUDA call): ABI version, element type, limits, operand
+ * dims/layout, program well-formedness (stack simulation: depth <= 8, exactly
+ * one result), op/type legality.  Usable without a GPU. */
+coot_status coot_validate(const coot_expr* e);
+
+/* out[i] = expr(i) for all i < n_rows*n_cols (one launch; zero if empty).
+ * `out` may equal an operand pointer exactly (B += 3*A); any other
+ * overlap with an operand is COOT_ERR_CONTRACT. */
+coot_status coot_eval(coot_ctx* ctx, const coot_expr* e, void* out);
+
+/* result <- reduce(kind, expr), in one launch.  If out_or_null is non-NULL
+ * the element-wise result is also written in the same pass ("Z = ...; then
+ * accu(Z)", R15) — full reductions only.  `result` must not overlap any
+ * operand or out.  Run-to-run deterministic: the grid and the combine order
+ * depend only on (n, pointer alignment, device SM count) (R14). */
+coot_status coot_reduce(coot_ctx* ctx, const coot_expr* e, uint32_t kind, void* result,
+                        void* out_or_null);
+
+/* Multi-GPU building blocks (contiguous-block sharding, R17).
+ * coot_reduce_partial writes this shard's UNROUNDED partial:
+ *   full reductions: one 32-byte record
+ *     ACCU/NORM2 (floats): {f64 sum (or sum of squares), -, u64 count, 0}
+ *     ACCU (ints):         {u64 modular sum,          -, u64 count, 0}
+ *     MIN/MAX/MINMAX:      {eT min bits, eT max bits,    u64 count, 0}
+ *   SUM_DIM0 / SUM_DIM1: len = n_cols / n_rows words (f64 for floats, u64 for ints).
+ * coot_combine reduces `nparts` such partials (laid out back to back, in rank
+ * order 0..nparts-1) in that fixed order and rounds once into `result` (same
+ * shape as coot_reduce).  `len` is the vector length for SUM_DIM*, else 1. */
+coot_status coot_reduce_partial(coot_ctx* ctx, const coot_expr* e, uint32_t kind,
+                                void* partial, void* out_or_null);
+coot_status coot_combine(coot_ctx* ctx, uint32_t elem, uint32_t kind, const void* partials,
+                         uint32_t nparts, uint64_t len, void* result);
+/* Bytes of one partial for (kind, len). Host-only. */
+coot_status coot_partial_bytes(uint32_t kind, uint64_t len, uint64_t* bytes);
+/* Contiguous block of [0, n) owned by `rank` of `nranks`:
+ * begin = floor(rank*n/nranks) rounded down to a multiple of `align` (ends are
+ * exact: rank 0 begins at 0, the last rank ends at n).  Host-only. */
+coot_status coot_shard_range(uint64_t n, uint32_t rank, uint32_t nranks, uint64_t align,
+                             uint64_t* begin, uint64_t* end);
+
+/* Synthetic inputs (fill::randu, and structured fills for closed
+ * forms): out[i] = f(global index start+i) of an operand with n_rows rows,
+ * stream = operand index, using the counter-based SplitMix64 recipe of
+ * DESIGN.md "Input recipe".  kinds: 0 randu, 1 ones, 2 iota, 3 i mod k,
+ * 4 column index, 5 row index, 6 zeros.  One launch. */
+coot_status coot_fill(coot_ctx* ctx, uint32_t elem, uint32_t fill_kind, uint64_t seed,
+                      uint64_t stream, uint64_t start, uint64_t count, uint64_t n_rows,
+                      uint64_t k, void* out);
+
+/* Synchronise the ctx stream; returns COOT_ERR_DEVICE on an async fault. */
+coot_status coot_sync(coot_ctx* ctx);
+
+const char* coot_status_string(coot_status s);
+/* Thread-local message of the last failing call in this thread ("" if none). */
+const char* coot_last_error(void);
+uint32_t coot_abi_version(void);
+
+typedef struct {
+  uint64_t launches;       /* kernels this ctx launched                         */
+  int32_t last_path;       /* catalog id >= 0, -1 interpreter, -2 dim kernel, -3 other */
+  uint32_t last_grid;      /* blocks of the last launch                          */
+  uint64_t last_alg_bytes; /* algorithmic HBM bytes of the last call             */
+  int32_t sm_count;
+  int32_t reserved;
+} coot_stats_t;
+coot_status coot_stats(const coot_ctx* ctx, coot_stats_t* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* COOT_H */

@@ -1,0 +1,455 @@
+"""Python front end: a ctx wrapper and an Armadillo/Bandicoot-style expression
+builder with delayed evaluation.
+
+Delayed evaluation (§3): operators only build an
+expression tree (the analogue of the eOp/eGlue compound types);
+nothing runs on the device until the expression is assigned (``eval``,
+``assign``) or reduced (``accu``, ``sum``, ``dot``, ``norm2``, ``min``,
+``max``).  At that point the tree is lowered to a postfix ``coot_expr`` and
+handed to ONE libcoot call.  Matrices are dense column-major
+(R2); ``Col`` is n x 1 and ``Row`` is 1 x n.
+
+torch is used only for device memory and streams; every element of every
+step is computed by libcoot's CUDA kernels.
+"""
+from __future__ import annotations
+
+import ctypes
+import numbers
+
+import torch
+
+from . import _native as N
+from ._native import CootError, check, lib
+
+TORCH_DTYPE = {"f32": torch.float32, "f64": torch.float64, "u32": torch.uint32,
+               "s64": torch.int64}
+ELEM_OF = {v: k for k, v in TORCH_DTYPE.items()}
+ESIZE = {"f32": 4, "f64": 8, "u32": 4, "s64": 8}
+
+
+def elem_of(t: torch.Tensor) -> str:
+    try:
+        return ELEM_OF[t.dtype]
+    except KeyError:
+        raise CootError(5, f"contract: unsupported dtype {t.dtype}") from None
+
+
+# ============================================================================
+# ctx
+# ============================================================================
+class Context:
+    """A libcoot ctx bound to (device, stream) — coot_init."""
+
+    def __init__(self, device: int = 0, stream: torch.cuda.Stream | None = None,
+                 flags: int = 0):
+        self.device_index = int(device)
+        self.device = torch.device("cuda", self.device_index)
+        self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
+        h = ctypes.c_void_p()
+        check(lib.coot_init(ctypes.byref(h), self.device_index,
+                            ctypes.c_void_p(self.stream.cuda_stream), flags))
+        self._h = h
+
+    @property
+    def handle(self):
+        if self._h is None:
+            raise CootError(1, "configuration: ctx is closed")
+        return self._h
+
+    def close(self):
+        if getattr(self, "_h", None) is not None:
+            check(lib.coot_destroy(self._h))
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()
+
+    def set_stream(self, stream: torch.cuda.Stream):
+        check(lib.coot_set_stream(self.handle, ctypes.c_void_p(stream.cuda_stream)))
+        self.stream = stream
+
+    # ---- program-level entry points (what tests and bench.py call) --------
+    def eval(self, elem, n_rows, n_cols, program, operands, scalars, out: torch.Tensor):
+        e = N.make_expr(elem, n_rows, n_cols, program, operands, scalars)
+        check(lib.coot_eval(self.handle, ctypes.byref(e), ctypes.c_void_p(out.data_ptr())))
+
+    def reduce(self, elem, n_rows, n_cols, program, operands, scalars, kind,
+               result: torch.Tensor, out: torch.Tensor | None = None):
+        e = N.make_expr(elem, n_rows, n_cols, program, operands, scalars)
+        check(lib.coot_reduce(self.handle, ctypes.byref(e), N.KIND[kind],
+                              ctypes.c_void_p(result.data_ptr()),
+                              ctypes.c_void_p(out.data_ptr() if out is not None else 0)))
+
+    def reduce_partial(self, elem, n_rows, n_cols, program, operands, scalars, kind,
+                       partial: torch.Tensor, out: torch.Tensor | None = None):
+        e = N.make_expr(elem, n_rows, n_cols, program, operands, scalars)
+        check(lib.coot_reduce_partial(self.handle, ctypes.byref(e), N.KIND[kind],
+                                      ctypes.c_void_p(partial.data_ptr()),
+                                      ctypes.c_void_p(out.data_ptr() if out is not None else 0)))
+
+    def combine(self, elem, kind, partials: torch.Tensor, nparts: int, length: int,
+                result: torch.Tensor):
+        check(lib.coot_combine(self.handle, N.ELEM[elem], N.KIND[kind],
+                               ctypes.c_void_p(partials.data_ptr()), nparts, length,
+                               ctypes.c_void_p(result.data_ptr())))
+
+    def fill(self, out: torch.Tensor, kind: str = "randu", *, seed: int = 42, stream: int = 0,
+             start: int = 0, n_rows: int = 1, k: int = 1):
+        check(lib.coot_fill(self.handle, N.ELEM[elem_of(out)], N.FILL[kind], seed, stream, start,
+                            out.numel(), n_rows, k, ctypes.c_void_p(out.data_ptr())))
+
+    def sync(self):
+        check(lib.coot_sync(self.handle))
+
+    def stats(self) -> dict:
+        s = N.Stats()
+        check(lib.coot_stats(self.handle, ctypes.byref(s)))
+        return {"launches": s.launches, "last_path": s.last_path, "last_grid": s.last_grid,
+                "last_alg_bytes": s.last_alg_bytes, "sm_count": s.sm_count}
+
+
+_default: dict[int, Context] = {}
+
+
+def init(device: int = 0, print_info: bool = False) -> Context:
+    """coot_init analogue: the default ctx for `device`."""
+    if device not in _default:
+        _default[device] = Context(device, flags=N.INIT_PRINT_INFO if print_info else 0)
+    return _default[device]
+
+
+def default_ctx(device: int | None = None) -> Context:
+    if device is None:
+        device = torch.cuda.current_device()
+    return init(device)
+
+
+def partial_bytes(kind: str, length: int = 1) -> int:
+    b = ctypes.c_uint64()
+    check(lib.coot_partial_bytes(N.KIND[kind], length, ctypes.byref(b)))
+    return int(b.value)
+
+
+def shard_range(n: int, rank: int, nranks: int, align: int = 1) -> tuple[int, int]:
+    """Contiguous block of [0, n) owned by `rank` (reading R17)."""
+    b, e = ctypes.c_uint64(), ctypes.c_uint64()
+    check(lib.coot_shard_range(n, rank, nranks, align, ctypes.byref(b), ctypes.byref(e)))
+    return int(b.value), int(e.value)
+
+
+def validate(elem, n_rows, n_cols, program, operands, scalars=()):
+    """Host-only descriptor validation (no GPU needed)."""
+    e = N.make_expr(elem, n_rows, n_cols, program, operands, scalars)
+    check(lib.coot_validate(ctypes.byref(e)))
+
+
+# ============================================================================
+# expression builder (delayed evaluation)
+# ============================================================================
+class Expr:
+    """Base of every matrix / vector / expression object (cf. Base<eT,T1>)."""
+
+    elem: str
+    n_rows: int
+    n_cols: int
+
+    # element-wise binary (eGlue) and scalar (eOp) operators
+    def __add__(self, o):
+        return _binary("ADD", self, o)
+
+    def __radd__(self, o):
+        return _binary("ADD", o, self)
+
+    def __sub__(self, o):
+        return _binary("SUB", self, o)
+
+    def __rsub__(self, o):
+        return _binary("SUB", o, self)
+
+    def __mul__(self, o):
+        if isinstance(o, Expr):
+            raise NotImplementedError(
+                "matrix product (Glue<...,glue_times>) is out of scope; use % for the Schur product")
+        return _binary("MUL", self, o)
+
+    def __rmul__(self, o):
+        if isinstance(o, Expr):
+            raise NotImplementedError("matrix product is out of scope")
+        return _binary("MUL", o, self)
+
+    def __mod__(self, o):  # Schur product (reading R1)
+        return _binary("MUL", self, o)
+
+    def __rmod__(self, o):
+        return _binary("MUL", o, self)
+
+    def __truediv__(self, o):
+        return _binary("DIV", self, o)
+
+    def __rtruediv__(self, o):
+        return _binary("DIV", o, self)
+
+    def __neg__(self):
+        return Node("NEG", (self,))
+
+    @property
+    def n_elem(self) -> int:
+        return self.n_rows * self.n_cols
+
+    # ---- evaluation ------------------------------------------------------
+    def eval(self, ctx: Context | None = None, out: "Mat | None" = None) -> "Mat":
+        """Assign the expression to a (new or given) matrix: ONE launch."""
+        lw = lower(self)
+        ctx = ctx or default_ctx(lw.device_index())
+        if out is None:
+            out = Mat.empty(lw.n_rows, lw.n_cols, lw.elem, device=lw.device())
+        elif (out.n_rows, out.n_cols, out.elem) != (lw.n_rows, lw.n_cols, lw.elem):
+            raise CootError(2, f"conformability: assignment target is {out.n_rows}x{out.n_cols} "
+                               f"{out.elem}, expression is {lw.n_rows}x{lw.n_cols} {lw.elem}")
+        ctx.eval(lw.elem, lw.n_rows, lw.n_cols, lw.program, lw.operands, lw.scalars, out.data)
+        return out
+
+
+class Mat(Expr):
+    """Dense column-major matrix held in a flat device tensor (Mat<eT>)."""
+
+    def __init__(self, data: torch.Tensor, n_rows: int, n_cols: int):
+        if data.dim() != 1 or not data.is_contiguous():
+            raise CootError(5, "contract: Mat data must be a contiguous 1-D tensor "
+                               "(column-major element order)")
+        if data.numel() != n_rows * n_cols:
+            raise CootError(2, f"conformability: {data.numel()} elements for {n_rows}x{n_cols}")
+        self.data = data
+        self.elem = elem_of(data)
+        self.n_rows, self.n_cols = int(n_rows), int(n_cols)
+
+    @classmethod
+    def empty(cls, n_rows, n_cols, elem="f32", device="cuda"):
+        return cls(torch.empty(n_rows * n_cols, dtype=TORCH_DTYPE[elem], device=device),
+                   n_rows, n_cols)
+
+    @classmethod
+    def from_torch(cls, t: torch.Tensor):
+        """Copy a (rows x cols) torch matrix (or 1-D vector -> Col) into column-major."""
+        if t.dim() == 1:
+            return cls(t.contiguous(), t.numel(), 1)
+        r, c = t.shape
+        return cls(t.t().contiguous().reshape(-1), r, c)
+
+    @classmethod
+    def randu(cls, n_rows, n_cols, elem="f32", *, seed=42, stream=0, ctx: Context | None = None,
+              device=None):
+        """fill::randu: uniform [0,1) from the counter-based recipe."""
+        ctx = ctx or default_ctx(device)
+        m = cls.empty(n_rows, n_cols, elem, device=ctx.device)
+        ctx.fill(m.data, "randu", seed=seed, stream=stream, n_rows=n_rows)
+        return m
+
+    @classmethod
+    def fill(cls, n_rows, n_cols, kind, elem="f32", *, seed=42, stream=0, k=1,
+             ctx: Context | None = None, device=None):
+        ctx = ctx or default_ctx(device)
+        m = cls.empty(n_rows, n_cols, elem, device=ctx.device)
+        ctx.fill(m.data, kind, seed=seed, stream=stream, n_rows=n_rows, k=k)
+        return m
+
+    def to_torch(self) -> torch.Tensor:
+        """(rows x cols) row-major view copy of the column-major data."""
+        return self.data.reshape(self.n_cols, self.n_rows).t()
+
+    def assign(self, e: Expr, ctx: Context | None = None) -> "Mat":
+        """self = e (exact aliasing with an operand is allowed: B += 3*A)."""
+        return as_expr(e, self.elem).eval(ctx, out=self)
+
+    def __iadd__(self, o):
+        return self.assign(self + o)
+
+    def __isub__(self, o):
+        return self.assign(self - o)
+
+    def __imod__(self, o):
+        return self.assign(self % o)
+
+    def __imul__(self, o):
+        return self.assign(self * o)
+
+    def __itruediv__(self, o):
+        return self.assign(self / o)
+
+
+def Col(data: torch.Tensor) -> Mat:
+    return Mat(data, data.numel(), 1)
+
+
+def Row(data: torch.Tensor) -> Mat:
+    return Mat(data, 1, data.numel())
+
+
+class ScalarLeaf(Expr):
+    def __init__(self, value):
+        self.value = value
+        self.elem = None
+        self.n_rows = self.n_cols = None
+
+
+class Node(Expr):
+    def __init__(self, op: str, kids: tuple):
+        self.op = op
+        self.kids = kids
+        mats = [k for k in kids if not isinstance(k, ScalarLeaf)]
+        ref = mats[0]
+        self.elem = ref.elem
+        self.n_rows, self.n_cols = ref.n_rows, ref.n_cols
+        for k in mats[1:]:
+            if k.elem != ref.elem:
+                raise CootError(5, f"contract: mixed element types {ref.elem} and {k.elem} in {op}")
+        self._mats = mats
+
+
+def as_expr(x, elem=None):
+    if isinstance(x, Expr):
+        return x
+    if isinstance(x, numbers.Number):
+        return ScalarLeaf(x)
+    raise TypeError(f"cannot use {type(x).__name__} in a coot expression")
+
+
+def _binary(op, a, b):
+    a, b = as_expr(a), as_expr(b)
+    if isinstance(a, ScalarLeaf) and isinstance(b, ScalarLeaf):
+        raise TypeError("scalar-only expression")
+    return Node(op, (a, b))
+
+
+def _unary(op, a):
+    a = as_expr(a)
+    if isinstance(a, ScalarLeaf):
+        raise TypeError("scalar-only expression")
+    return Node(op, (a,))
+
+
+def exp(x): return _unary("EXP", x)
+def log(x): return _unary("LOG", x)
+def sqrt(x): return _unary("SQRT", x)
+def abs(x): return _unary("ABS", x)  # noqa: A001
+def square(x): return _unary("SQUARE", x)
+
+
+class Lowered:
+    def __init__(self, elem, n_rows, n_cols, program, operands, scalars):
+        self.elem, self.n_rows, self.n_cols = elem, n_rows, n_cols
+        self.program, self.operands, self.scalars = program, operands, scalars
+
+    def device(self):
+        return self.operands[0].device
+
+    def device_index(self):
+        return self.operands[0].device.index
+
+
+def lower(e: Expr) -> Lowered:
+    """Tree -> postfix program.  Operands are deduplicated by identity of their
+    storage (each distinct array is loaded once); scalars by value."""
+    if isinstance(e, ScalarLeaf):
+        raise TypeError("scalar-only expression")
+    operands: list[torch.Tensor] = []
+    op_index: dict[int, int] = {}
+    scalars: list = []
+    program: list[tuple[str, int]] = []
+    elem, nr, nc = e.elem, e.n_rows, e.n_cols
+
+    def visit(x):
+        if isinstance(x, Mat):
+            if (x.n_rows, x.n_cols) != (nr, nc):
+                raise CootError(2, f"conformability: operand is {x.n_rows}x{x.n_cols}, "
+                                   f"expression is {nr}x{nc}")
+            key = x.data.data_ptr()
+            if key not in op_index:
+                op_index[key] = len(operands)
+                operands.append(x.data)
+            program.append(("LOAD", op_index[key]))
+        elif isinstance(x, ScalarLeaf):
+            v = x.value
+            if elem in ("u32", "s64") and isinstance(v, float) and not float(v).is_integer():
+                raise CootError(5, f"contract: scalar {v!r} is not integral for a {elem} expression")
+            for i, s in enumerate(scalars):
+                if type(s) is type(v) and s == v:
+                    program.append(("SCALAR", i))
+                    break
+            else:
+                scalars.append(v)
+                program.append(("SCALAR", len(scalars) - 1))
+        else:
+            if (x.n_rows, x.n_cols) != (nr, nc):
+                raise CootError(2, f"conformability: {x.op} operand is {x.n_rows}x{x.n_cols}, "
+                                   f"expression is {nr}x{nc}")
+            for k in x.kids:
+                visit(k)
+            program.append((x.op, 0))
+
+    visit(e)
+    return Lowered(elem, nr, nc, program, operands, scalars)
+
+
+# ---- terminal reductions ----------------------------------------------------
+def _reduce(e, kind, ctx=None, out: Mat | None = None):
+    lw = lower(as_expr(e))
+    ctx = ctx or default_ctx(lw.device_index())
+    shape = {"MINMAX": (2,), "SUM_DIM0": (lw.n_cols,), "SUM_DIM1": (lw.n_rows,)}.get(kind, (1,))
+    result = torch.empty(shape, dtype=TORCH_DTYPE[lw.elem], device=lw.device())
+    ctx.reduce(lw.elem, lw.n_rows, lw.n_cols, lw.program, lw.operands, lw.scalars, kind, result,
+               out.data if out is not None else None)
+    return result
+
+
+def accu(e, ctx=None, out: Mat | None = None) -> torch.Tensor:
+    """Sum of all elements (``float result = sum(A)``); 1-element device tensor."""
+    return _reduce(e, "ACCU", ctx, out)
+
+
+def sum(e, dim: int | None = None, ctx=None):  # noqa: A001
+    """Armadillo sum: dim 0 -> column sums (Row), dim 1 -> row sums (Col) (R3);
+    for a vector with dim=None the sum of all elements."""
+    e = as_expr(e)
+    if dim is None:
+        if e.n_rows == 1 or e.n_cols == 1:
+            return accu(e, ctx)
+        dim = 0
+    r = _reduce(e, "SUM_DIM0" if dim == 0 else "SUM_DIM1", ctx)
+    return Mat(r, 1, r.numel()) if dim == 0 else Mat(r, r.numel(), 1)
+
+
+def dot(a, b, ctx=None):
+    """dot(x, y) = accu(x % y) with eT-rounded products (reading R11)."""
+    return accu(as_expr(a) % as_expr(b), ctx)
+
+
+def norm2(e, ctx=None):
+    return _reduce(e, "NORM2", ctx)
+
+
+def min(a, b=None, ctx=None):  # noqa: A001
+    """min(X): smallest element (reduction); min(A, B): element-wise."""
+    if b is not None:
+        return _binary("MIN", a, b)
+    return _reduce(a, "MIN", ctx)
+
+
+def max(a, b=None, ctx=None):  # noqa: A001
+    if b is not None:
+        return _binary("MAX", a, b)
+    return _reduce(a, "MAX", ctx)
+
+
+def minmax(e, ctx=None):
+    return _reduce(e, "MINMAX", ctx)

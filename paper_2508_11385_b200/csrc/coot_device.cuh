@@ -1,0 +1,483 @@
+// Device-side building blocks shared by every libcoot kernel (sm_100a):
+// element semantics per opcode and type, 16-byte streaming loads/stores,
+// per-thread accumulators and the fixed-order (deterministic) block and
+// final reductions.
+//
+// Numerics (readings R5-R10):
+//  * every node rounds to eT, no FMA contraction: explicit __f*_rn / __d*_rn
+//    intrinsics (and the build uses -fmad=false, no FTZ, IEEE div/sqrt), so
+//    + - * / sqrt are bit-identical to the eager oracle;
+//  * f32 EXP/LOG are computed in f64 and rounded once (correctly rounded
+//    except in ~2^-28 of cases); f64 EXP/LOG use CUDA exp/log (<= 1 ulp);
+//  * f32 reductions: 16-byte unit (4 elements) summed pairwise in f32, then
+//    accumulated in f64; the final value is rounded once to eT;
+//  * integers: modular (u64 accumulator, truncated at the end).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/coot.h"
+
+namespace coot {
+
+typedef long long s64;
+typedef unsigned long long u64;
+
+enum AccKind { ACC_NONE = 0, ACC_SUM = 1, ACC_SUMSQ = 2, ACC_MINMAX = 3 };
+enum FinalMode { FINAL_ROUND = 0, FINAL_PARTIAL = 1 };
+
+constexpr int kThreads = 256;
+constexpr int kWarps = kThreads / 32;
+
+// One reduction partial record (COOT_PARTIAL_BYTES = 32).
+struct __align__(16) Rec {
+  u64 a, b, count, pad;
+};
+
+// Kernel arguments for the fused element-wise pass (passed as a
+// __grid_constant__ parameter; < 1 KB).
+struct FusedArgs {
+  const void* in[COOT_MAX_OPERANDS];
+  void* out;          // element-wise result or nullptr
+  u64 n;              // elements
+  u64 head;           // scalar elements before the 16-byte aligned body
+  u64 nunits;         // 16-byte units in the body
+  u64 tail_begin;     // = head + nunits * W
+  u64 scalars[COOT_MAX_SCALARS];  // eT bits
+  Rec* partials;      // per-block records (ctx scratch)
+  unsigned* ticket;   // self-resetting arrival counter (ctx scratch)
+  void* result;       // eT result(s) or a Rec (FINAL_PARTIAL)
+  u64 count;          // element count recorded in a partial
+  uint32_t final_mode;
+  uint32_t kind;      // coot_reduce_kind
+  uint32_t n_operands;
+  uint32_t n_instr;
+  uint16_t key[COOT_MAX_INSTR];  // interpreter: (op << 8) | (depth << 4) | arg
+  uint8_t arg[COOT_MAX_INSTR];
+};
+
+template <class T>
+struct Unit {
+  static constexpr int W = 16 / sizeof(T);
+};
+
+// ---- scalar slot decoding -------------------------------------------------
+template <class T>
+__device__ __forceinline__ T scalar_as(u64 bits);
+template <>
+__device__ __forceinline__ float scalar_as<float>(u64 bits) {
+  return __uint_as_float((unsigned)bits);
+}
+template <>
+__device__ __forceinline__ double scalar_as<double>(u64 bits) {
+  return __longlong_as_double((long long)bits);
+}
+template <>
+__device__ __forceinline__ uint32_t scalar_as<uint32_t>(u64 bits) {
+  return (uint32_t)bits;
+}
+template <>
+__device__ __forceinline__ s64 scalar_as<s64>(u64 bits) {
+  return (s64)bits;
+}
+
+template <class T>
+__device__ __forceinline__ u64 to_bits(T v);
+template <>
+__device__ __forceinline__ u64 to_bits<float>(float v) {
+  return (u64)__float_as_uint(v);
+}
+template <>
+__device__ __forceinline__ u64 to_bits<double>(double v) {
+  return (u64)__double_as_longlong(v);
+}
+template <>
+__device__ __forceinline__ u64 to_bits<uint32_t>(uint32_t v) {
+  return (u64)v;
+}
+template <>
+__device__ __forceinline__ u64 to_bits<s64>(s64 v) {
+  return (u64)v;
+}
+
+template <class T>
+__host__ __device__ constexpr bool is_float() {
+  return T(0.5) != T(0);
+}
+
+// ---- op legality (R9) -----------------------------------------------------
+template <class T>
+__host__ __device__ constexpr bool op_legal(int op) {
+  return is_float<T>() ? true
+                       : !(op == COOT_OP_SQRT || op == COOT_OP_EXP || op == COOT_OP_LOG ||
+                           op == COOT_OP_DIV);
+}
+
+// ---- element semantics ------------------------------------------------------
+template <int OP>
+__device__ __forceinline__ float un(float a) {
+  if constexpr (OP == COOT_OP_NEG) return -a;
+  else if constexpr (OP == COOT_OP_ABS) return fabsf(a);
+  else if constexpr (OP == COOT_OP_SQUARE) return __fmul_rn(a, a);
+  else if constexpr (OP == COOT_OP_SQRT) return __fsqrt_rn(a);
+  // f32 EXP/LOG are evaluated in f64 (B200 runs FP64 at half the FP32 rate)
+  // and rounded once: the f64 result is within 1 ulp(f64), so the f32 result
+  // is the correctly rounded one except when exp(x)/log(x) lies within
+  // ~2^-52 relative of an f32 rounding boundary (R6).  This keeps
+  // composed expressions bit-identical to the correctly-rounded oracle, where
+  // expf/logf (<= 2 / 1 ulp) would let later nodes amplify the difference.
+  else if constexpr (OP == COOT_OP_EXP) return __double2float_rn(exp((double)a));
+  else if constexpr (OP == COOT_OP_LOG) return __double2float_rn(log((double)a));
+  else return a;
+}
+template <int OP>
+__device__ __forceinline__ double un(double a) {
+  if constexpr (OP == COOT_OP_NEG) return -a;
+  else if constexpr (OP == COOT_OP_ABS) return fabs(a);
+  else if constexpr (OP == COOT_OP_SQUARE) return __dmul_rn(a, a);
+  else if constexpr (OP == COOT_OP_SQRT) return __dsqrt_rn(a);
+  else if constexpr (OP == COOT_OP_EXP) return exp(a);
+  else if constexpr (OP == COOT_OP_LOG) return log(a);
+  else return a;
+}
+template <int OP>
+__device__ __forceinline__ uint32_t un(uint32_t a) {
+  if constexpr (OP == COOT_OP_NEG) return 0u - a;
+  else if constexpr (OP == COOT_OP_SQUARE) return a * a;
+  else return a;  // ABS of unsigned is the identity; illegal ops never reach here
+}
+template <int OP>
+__device__ __forceinline__ s64 un(s64 a) {
+  const u64 x = (u64)a;
+  if constexpr (OP == COOT_OP_NEG) return (s64)(0ull - x);
+  else if constexpr (OP == COOT_OP_ABS) return a < 0 ? (s64)(0ull - x) : a;
+  else if constexpr (OP == COOT_OP_SQUARE) return (s64)(x * x);
+  else return a;
+}
+
+template <int OP>
+__device__ __forceinline__ float bin(float a, float b) {
+  if constexpr (OP == COOT_OP_ADD) return __fadd_rn(a, b);
+  else if constexpr (OP == COOT_OP_SUB) return __fsub_rn(a, b);
+  else if constexpr (OP == COOT_OP_MUL) return __fmul_rn(a, b);
+  else if constexpr (OP == COOT_OP_DIV) return __fdiv_rn(a, b);
+  else if constexpr (OP == COOT_OP_MIN) return (b < a) ? b : a;
+  else if constexpr (OP == COOT_OP_MAX) return (a < b) ? b : a;
+  else return a;
+}
+template <int OP>
+__device__ __forceinline__ double bin(double a, double b) {
+  if constexpr (OP == COOT_OP_ADD) return __dadd_rn(a, b);
+  else if constexpr (OP == COOT_OP_SUB) return __dsub_rn(a, b);
+  else if constexpr (OP == COOT_OP_MUL) return __dmul_rn(a, b);
+  else if constexpr (OP == COOT_OP_DIV) return __ddiv_rn(a, b);
+  else if constexpr (OP == COOT_OP_MIN) return (b < a) ? b : a;
+  else if constexpr (OP == COOT_OP_MAX) return (a < b) ? b : a;
+  else return a;
+}
+template <int OP>
+__device__ __forceinline__ uint32_t bin(uint32_t a, uint32_t b) {
+  if constexpr (OP == COOT_OP_ADD) return a + b;
+  else if constexpr (OP == COOT_OP_SUB) return a - b;
+  else if constexpr (OP == COOT_OP_MUL) return a * b;
+  else if constexpr (OP == COOT_OP_MIN) return (b < a) ? b : a;
+  else if constexpr (OP == COOT_OP_MAX) return (a < b) ? b : a;
+  else return a;
+}
+template <int OP>
+__device__ __forceinline__ s64 bin(s64 a, s64 b) {
+  const u64 x = (u64)a, y = (u64)b;
+  if constexpr (OP == COOT_OP_ADD) return (s64)(x + y);
+  else if constexpr (OP == COOT_OP_SUB) return (s64)(x - y);
+  else if constexpr (OP == COOT_OP_MUL) return (s64)(x * y);
+  else if constexpr (OP == COOT_OP_MIN) return (b < a) ? b : a;
+  else if constexpr (OP == COOT_OP_MAX) return (a < b) ? b : a;
+  else return a;
+}
+
+// ---- 16-byte streaming memory access --------------------------------------
+// Coherent loads (an operand may alias `out` exactly), no L1 allocation
+// (each byte is touched once); the element-wise output is stored with the
+// evict-first (.cs) hint.
+__device__ __forceinline__ uint4 ld16(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.L1::no_allocate.v4.b32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+__device__ __forceinline__ void st16(void* p, uint4 v) {
+  asm volatile("st.global.cs.v4.b32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y),
+               "r"(v.z), "r"(v.w)
+               : "memory");
+}
+
+template <class T>
+__device__ __forceinline__ void load_unit(const T* p, T (&v)[Unit<T>::W]) {
+  uint4 r = ld16(p);
+  static_assert(sizeof(v) == 16, "unit is 16 bytes");
+  memcpy(&v[0], &r, 16);
+}
+template <class T>
+__device__ __forceinline__ void store_unit(T* p, const T (&v)[Unit<T>::W]) {
+  uint4 r;
+  memcpy(&r, &v[0], 16);
+  st16(p, r);
+}
+
+// ---- warp shuffles for 64-bit values ---------------------------------------
+__device__ __forceinline__ double shfl_xor(double v, int m) {
+  return __shfl_xor_sync(0xffffffffu, v, m);
+}
+__device__ __forceinline__ u64 shfl_xor(u64 v, int m) {
+  return (u64)__shfl_xor_sync(0xffffffffu, (long long)v, m);
+}
+__device__ __forceinline__ float shfl_xor(float v, int m) {
+  return __shfl_xor_sync(0xffffffffu, v, m);
+}
+__device__ __forceinline__ uint32_t shfl_xor(uint32_t v, int m) {
+  return __shfl_xor_sync(0xffffffffu, v, m);
+}
+__device__ __forceinline__ s64 shfl_xor(s64 v, int m) {
+  return __shfl_xor_sync(0xffffffffu, v, m);
+}
+
+// ---- per-thread accumulators -------------------------------------------------
+template <class T>
+struct MinMaxId;
+template <>
+struct MinMaxId<float> {
+  __device__ static float lo() { return __int_as_float(0x7f800000); }   // +inf
+  __device__ static float hi() { return __int_as_float((int)0xff800000u); }  // -inf
+};
+template <>
+struct MinMaxId<double> {
+  __device__ static double lo() { return __longlong_as_double(0x7ff0000000000000ll); }
+  __device__ static double hi() { return __longlong_as_double((long long)0xfff0000000000000ull); }
+};
+template <>
+struct MinMaxId<uint32_t> {
+  __device__ static uint32_t lo() { return 0xffffffffu; }
+  __device__ static uint32_t hi() { return 0u; }
+};
+template <>
+struct MinMaxId<s64> {
+  __device__ static s64 lo() { return 0x7fffffffffffffffll; }
+  __device__ static s64 hi() { return (s64)0x8000000000000000ull; }
+};
+
+// Sum type: f64 for floats, u64 (modular) for integers.
+template <class T>
+struct SumT {
+  typedef double type;
+};
+template <>
+struct SumT<uint32_t> {
+  typedef u64 type;
+};
+template <>
+struct SumT<s64> {
+  typedef u64 type;
+};
+
+template <class S>
+__device__ __forceinline__ S sum_add(S a, S b);
+template <>
+__device__ __forceinline__ double sum_add<double>(double a, double b) {
+  return __dadd_rn(a, b);
+}
+template <>
+__device__ __forceinline__ u64 sum_add<u64>(u64 a, u64 b) {
+  return a + b;
+}
+
+// Pairwise sum of a unit (or one element) in eT, then widened.  For f32 the
+// unit of 4 is ((v0+v1)+(v2+v3)) in f32 — one f32->f64 conversion per unit.
+template <class T, int W>
+__device__ __forceinline__ typename SumT<T>::type unit_sum(const T (&v)[W]) {
+  if constexpr (is_float<T>()) {
+    if constexpr (W == 1) {
+      return (double)v[0];
+    } else if constexpr (W == 2) {
+      return (double)bin<COOT_OP_ADD>(v[0], v[1]);
+    } else {
+      static_assert(W == 4, "unit");
+      return (double)bin<COOT_OP_ADD>(bin<COOT_OP_ADD>(v[0], v[1]), bin<COOT_OP_ADD>(v[2], v[3]));
+    }
+  } else {
+    u64 s = 0;
+#pragma unroll
+    for (int w = 0; w < W; ++w) s += (u64)v[w];
+    return s;
+  }
+}
+
+template <class T, int ACC>
+struct Accum {
+  typedef typename SumT<T>::type S;
+  S s;
+  T mn, mx;
+  __device__ __forceinline__ void init() {
+    s = S(0);
+    mn = MinMaxId<T>::lo();
+    mx = MinMaxId<T>::hi();
+  }
+  template <int W>
+  __device__ __forceinline__ void add(const T (&v)[W]) {
+    if constexpr (ACC == ACC_SUM) {
+      s = sum_add<S>(s, unit_sum<T, W>(v));
+    } else if constexpr (ACC == ACC_SUMSQ) {
+      T q[W];
+#pragma unroll
+      for (int w = 0; w < W; ++w) q[w] = bin<COOT_OP_MUL>(v[w], v[w]);
+      s = sum_add<S>(s, unit_sum<T, W>(q));
+    } else if constexpr (ACC == ACC_MINMAX) {
+#pragma unroll
+      for (int w = 0; w < W; ++w) {
+        mn = bin<COOT_OP_MIN>(mn, v[w]);
+        mx = bin<COOT_OP_MAX>(mx, v[w]);
+      }
+    }
+  }
+  // Fixed xor-butterfly: every lane ends with the same value.
+  __device__ __forceinline__ void warp_reduce() {
+#pragma unroll
+    for (int m = 16; m >= 1; m >>= 1) {
+      if constexpr (ACC == ACC_SUM || ACC == ACC_SUMSQ) {
+        s = sum_add<S>(s, shfl_xor(s, m));
+      } else if constexpr (ACC == ACC_MINMAX) {
+        mn = bin<COOT_OP_MIN>(mn, shfl_xor(mn, m));
+        mx = bin<COOT_OP_MAX>(mx, shfl_xor(mx, m));
+      }
+    }
+  }
+  __device__ __forceinline__ void merge(const Accum& o) {
+    if constexpr (ACC == ACC_SUM || ACC == ACC_SUMSQ) {
+      s = sum_add<S>(s, o.s);
+    } else if constexpr (ACC == ACC_MINMAX) {
+      mn = bin<COOT_OP_MIN>(mn, o.mn);
+      mx = bin<COOT_OP_MAX>(mx, o.mx);
+    }
+  }
+  __device__ __forceinline__ Rec to_rec(u64 count) const {
+    Rec r;
+    if constexpr (ACC == ACC_MINMAX) {
+      r.a = to_bits<T>(mn);
+      r.b = to_bits<T>(mx);
+    } else if constexpr (is_float<T>()) {
+      r.a = (u64)__double_as_longlong((double)s);
+      r.b = 0;
+    } else {
+      r.a = (u64)s;
+      r.b = 0;
+    }
+    r.count = count;
+    r.pad = 0;
+    return r;
+  }
+  __device__ __forceinline__ void from_rec(const Rec& r) {
+    init();
+    if constexpr (ACC == ACC_MINMAX) {
+      // empty producers publish the identities (+inf/-inf, UINT_MAX/0, ...)
+      mn = scalar_as<T>(r.a);
+      mx = scalar_as<T>(r.b);
+    } else if constexpr (is_float<T>()) {
+      s = __longlong_as_double((long long)r.a);
+    } else {
+      s = r.a;
+    }
+  }
+};
+
+// Load a record written by another block of this grid (bypass L1).
+__device__ __forceinline__ Rec load_rec_cg(const Rec* p) {
+  Rec r;
+  r.a = __ldcg(&p->a);
+  r.b = __ldcg(&p->b);
+  r.count = __ldcg(&p->count);
+  r.pad = 0;
+  return r;
+}
+
+// Round the combined accumulator into the user-visible result (eT).
+template <class T, int ACC>
+__device__ __forceinline__ void write_final(const Accum<T, ACC>& acc, uint32_t kind, void* result) {
+  T* out = reinterpret_cast<T*>(result);
+  if constexpr (ACC == ACC_MINMAX) {
+    if (kind == COOT_RED_MIN) out[0] = acc.mn;
+    else if (kind == COOT_RED_MAX) out[0] = acc.mx;
+    else {
+      out[0] = acc.mn;
+      out[1] = acc.mx;
+    }
+  } else if constexpr (ACC == ACC_SUMSQ) {
+    if constexpr (sizeof(T) == 4) out[0] = __double2float_rn(__dsqrt_rn(acc.s));
+    else out[0] = (T)__dsqrt_rn(acc.s);
+  } else if constexpr (ACC == ACC_SUM) {
+    if constexpr (is_float<T>()) {
+      if constexpr (sizeof(T) == 4) out[0] = __double2float_rn(acc.s);
+      else out[0] = (T)acc.s;
+    } else {
+      out[0] = (T)acc.s;  // modular truncation for u32
+    }
+  }
+}
+
+// Block-level fixed-order reduction of per-thread accumulators; returns the
+// block total in thread 0 (other threads: unspecified).
+template <class T, int ACC>
+__device__ __forceinline__ Accum<T, ACC> block_reduce(Accum<T, ACC> acc) {
+  __shared__ Accum<T, ACC> ws[kWarps];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  acc.warp_reduce();
+  if (lane == 0) ws[warp] = acc;
+  __syncthreads();
+  Accum<T, ACC> r;
+  r.init();
+  if (warp == 0) {
+    if (lane < kWarps) r = ws[lane];
+    r.warp_reduce();
+  }
+  __syncthreads();
+  return r;
+}
+
+// Deterministic single-launch finish: every block publishes a record; the
+// last block to arrive (ticket) combines ALL records in block order
+// (lane-strided, then a fixed butterfly) and rounds once.  The ticket
+// self-resets so the next launch on the stream can reuse it.
+template <class T, int ACC>
+__device__ __forceinline__ void grid_finish(const Accum<T, ACC>& block_total, Rec* partials,
+                                            unsigned* ticket, uint32_t final_mode,
+                                            uint32_t kind, void* result, u64 count) {
+  __shared__ bool am_last;
+  if (threadIdx.x == 0) {
+    partials[blockIdx.x] = block_total.to_rec(0);
+    __threadfence();
+    const unsigned t = atomicAdd(ticket, 1u);
+    am_last = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!am_last) return;
+  __threadfence();
+  if (threadIdx.x < 32) {
+    Accum<T, ACC> acc;
+    acc.init();
+    for (unsigned b = threadIdx.x; b < gridDim.x; b += 32) {
+      Accum<T, ACC> o;
+      o.from_rec(load_rec_cg(&partials[b]));
+      acc.merge(o);
+    }
+    acc.warp_reduce();
+    if (threadIdx.x == 0) {
+      if (final_mode == FINAL_PARTIAL) {
+        *reinterpret_cast<Rec*>(result) = acc.to_rec(count);
+      } else {
+        write_final<T, ACC>(acc, kind, result);
+      }
+      *ticket = 0u;
+    }
+  }
+}
+
+}  // namespace coot

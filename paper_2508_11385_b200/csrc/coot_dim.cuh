@@ -1,0 +1,286 @@
+// K4 sum(X,0) and K5 sum(X,1) over a column-major m x n expression X
+// (Armadillo convention, R3: dim 0 -> column sums, a Row of n; dim 1 -> row
+// sums, a Col of m).  X may itself be a fused element-wise expression: every
+// element is produced by the same evaluators as the fused pass (K1 [L0] or
+// K2), so nothing is materialised.
+//
+// Both kernels are single-launch and deterministic: the split of the work
+// into (column, segment) / (row tile, column chunk) pieces depends only on
+// (m, n, SM count); split pieces publish unrounded partials that the LAST
+// arriving block (per column / per row tile, via a self-resetting ticket)
+// combines in fixed piece order before rounding once to eT.
+#pragma once
+#include "coot_fused.cuh"
+
+namespace coot {
+
+struct DimArgs {
+  FusedArgs f;          // operands, scalars, program (f.n unused)
+  u64 m, n;             // rows, cols
+  void* result;         // eT out (FINAL_ROUND) or S partial vector (FINAL_PARTIAL)
+  void* part;           // scratch: S partials of split pieces
+  unsigned* tickets;    // scratch: per column (dim0) / per row tile (dim1)
+  u64 seg_len;          // dim0: rows per segment (multiple of 4)
+  uint32_t nseg;        // dim0: segments per column (1 = no split)
+  uint32_t vec_ok;      // all operand columns 16-byte aligned alike
+  uint32_t final_mode;
+  uint32_t tpr;         // dim1: threads per row tile (32..256, power of two)
+  u64 ccols;            // dim1: columns per chunk
+  uint32_t nchunks;     // dim1: column chunks (1 = no split)
+  uint32_t nrt;         // dim1: row tiles
+};
+
+template <class T>
+__device__ __forceinline__ void store_dim_value(const DimArgs& d, u64 idx,
+                                                typename SumT<T>::type s) {
+  typedef typename SumT<T>::type S;
+  if (d.final_mode == FINAL_PARTIAL) {
+    reinterpret_cast<S*>(d.result)[idx] = s;
+  } else {
+    T v;
+    if constexpr (sizeof(T) == 4 && is_float<T>()) v = __double2float_rn(s);
+    else v = (T)s;
+    reinterpret_cast<T*>(d.result)[idx] = v;
+  }
+}
+
+// ---- K4a: block per (column, segment) — tall columns ------------------------
+template <class T, class EV>
+__global__ void __launch_bounds__(kThreads) dim0_block_kernel(const __grid_constant__ DimArgs d) {
+  constexpr int W = Unit<T>::W;
+  constexpr int K = EV::K;
+  typedef typename SumT<T>::type S;
+  const u64 npieces = d.n * d.nseg;
+  for (u64 p = blockIdx.x; p < npieces; p += gridDim.x) {
+    const u64 j = p / d.nseg, s = p % d.nseg;
+    const u64 r0 = s * d.seg_len;
+    const u64 len = (d.m - r0) < d.seg_len ? (d.m - r0) : d.seg_len;
+    const u64 e0 = j * d.m + r0;
+    u64 head = len, nun = 0;
+    if (d.vec_ok) {
+      const uintptr_t addr = reinterpret_cast<uintptr_t>(d.f.in[0]) + e0 * sizeof(T);
+      head = ((16 - (addr & 15)) & 15) / sizeof(T);
+      if (head > len) head = len;
+      nun = (len - head) / W;
+    }
+    const u64 tb = head + nun * W;
+    Accum<T, ACC_SUM> acc;
+    acc.init();
+    for (u64 i = threadIdx.x; i < head; i += kThreads) {
+      T in[K][1], v[1];
+      load_elem<T, EV>(d.f, e0 + i, in);
+      EV::template eval<T, 1>(in, d.f, v);
+      acc.template add<1>(v);
+    }
+    u64 u = threadIdx.x;
+    constexpr int UL = EV::kInterp ? 1 : 4;  // units whose loads are issued together
+    if constexpr (UL > 1) {
+      for (; u + (UL - 1) * kThreads < nun; u += UL * kThreads) {
+        T in[UL][K][W];
+#pragma unroll
+        for (int q = 0; q < UL; ++q)
+          load_units<T, EV>(d.f, e0 + head + (u + q * kThreads) * W, in[q]);
+#pragma unroll
+        for (int q = 0; q < UL; ++q) {
+          T v[W];
+          EV::template eval<T, W>(in[q], d.f, v);
+          acc.template add<W>(v);
+        }
+      }
+    }
+    for (; u < nun; u += kThreads) {
+      T in[K][W], v[W];
+      load_units<T, EV>(d.f, e0 + head + u * W, in);
+      EV::template eval<T, W>(in, d.f, v);
+      acc.template add<W>(v);
+    }
+    for (u64 i = tb + threadIdx.x; i < len; i += kThreads) {
+      T in[K][1], v[1];
+      load_elem<T, EV>(d.f, e0 + i, in);
+      EV::template eval<T, 1>(in, d.f, v);
+      acc.template add<1>(v);
+    }
+    Accum<T, ACC_SUM> bt = block_reduce<T, ACC_SUM>(acc);
+    if (d.nseg == 1) {
+      if (threadIdx.x == 0) store_dim_value<T>(d, j, bt.s);
+    } else {
+      __shared__ bool last;
+      if (threadIdx.x == 0) {
+        reinterpret_cast<S*>(d.part)[p] = bt.s;
+        __threadfence();
+        const unsigned t = atomicAdd(&d.tickets[j], 1u);
+        last = (t == d.nseg - 1);
+        if (last) {
+          __threadfence();
+          S tot = S(0);
+          for (uint32_t q = 0; q < d.nseg; ++q)
+            tot = sum_add<S>(tot, __ldcg(reinterpret_cast<const S*>(d.part) + j * d.nseg + q));
+          store_dim_value<T>(d, j, tot);
+          d.tickets[j] = 0u;
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// ---- K4b: warp per column — short columns (m < 2048) ------------------------
+template <class T, class EV>
+__global__ void __launch_bounds__(kThreads) dim0_warp_kernel(const __grid_constant__ DimArgs d) {
+  constexpr int K = EV::K;
+  const int lane = threadIdx.x & 31;
+  const u64 warp = ((u64)blockIdx.x * kThreads + threadIdx.x) >> 5;
+  const u64 nwarps = ((u64)gridDim.x * kThreads) >> 5;
+  for (u64 j = warp; j < d.n; j += nwarps) {
+    Accum<T, ACC_SUM> acc;
+    acc.init();
+    const u64 e0 = j * d.m;
+    for (u64 i = lane; i < d.m; i += 32) {
+      T in[K][1], v[1];
+      load_elem<T, EV>(d.f, e0 + i, in);
+      EV::template eval<T, 1>(in, d.f, v);
+      acc.template add<1>(v);
+    }
+    acc.warp_reduce();
+    if (lane == 0) store_dim_value<T>(d, j, acc.s);
+  }
+}
+
+// ---- K5: row sums — row tile x column chunk ---------------------------------
+// Block b -> row tile rt = b mod nrt, column chunk cc = b / nrt.  Threads form
+// G = 256/tpr groups; group g walks columns c0+g, c0+g+G, ... of the chunk and
+// each thread owns W consecutive rows (one 16-byte unit per column) of the
+// tile (vec path) or rows r0+q, r0+q+tpr, ... (scalar path).  Groups are
+// combined in g order through shared memory; chunks in cc order by the last
+// block of the row tile.
+template <class T, class EV>
+__global__ void __launch_bounds__(kThreads) dim1_kernel(const __grid_constant__ DimArgs d) {
+  constexpr int W = Unit<T>::W;
+  constexpr int K = EV::K;
+  typedef typename SumT<T>::type S;
+  __shared__ S red[kThreads * W];
+  __shared__ bool last;
+  const uint32_t tpr = d.tpr, G = kThreads / tpr;
+  const uint32_t g = threadIdx.x / tpr, q = threadIdx.x % tpr;
+  const u64 rt = blockIdx.x % d.nrt, cc = blockIdx.x / d.nrt;
+  const u64 R = (u64)tpr * W;
+  const u64 r0 = rt * R;
+  const u64 c0 = cc * d.ccols;
+  const u64 c1 = (c0 + d.ccols < d.n) ? c0 + d.ccols : d.n;
+  S acc[W];
+#pragma unroll
+  for (int w = 0; w < W; ++w) acc[w] = S(0);
+
+  // Uniform per block: a full tile uses the unit map, a ragged last tile the
+  // scalar map (both cover rows [r0, r0 + R) exactly once).
+  const bool vec_rows = d.vec_ok && (r0 + R <= d.m);
+  if (vec_rows) {
+    const u64 rbase = r0 + (u64)q * W;
+    u64 j = c0 + g;
+    for (; j + 3 * G < c1; j += 4 * G) {
+      T v[4][W];
+      if constexpr (!EV::kInterp) {
+        T in[4][K][W];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) load_units<T, EV>(d.f, (j + c * G) * d.m + rbase, in[c]);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) EV::template eval<T, W>(in[c], d.f, v[c]);
+      } else {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          T in[K][W];
+          load_units<T, EV>(d.f, (j + c * G) * d.m + rbase, in);
+          EV::template eval<T, W>(in, d.f, v[c]);
+        }
+      }
+#pragma unroll
+      for (int w = 0; w < W; ++w) {
+        T col4[4] = {v[0][w], v[1][w], v[2][w], v[3][w]};
+        if constexpr (is_float<T>()) {
+          acc[w] = sum_add<S>(acc[w], unit_sum<T, 4>(col4));
+        } else {
+#pragma unroll
+          for (int c = 0; c < 4; ++c) acc[w] = sum_add<S>(acc[w], (S)col4[c]);
+        }
+      }
+    }
+    for (; j < c1; j += G) {
+      T in[K][W], v[W];
+      load_units<T, EV>(d.f, j * d.m + rbase, in);
+      EV::template eval<T, W>(in, d.f, v);
+#pragma unroll
+      for (int w = 0; w < W; ++w) {
+        T one[1] = {v[w]};
+        acc[w] = sum_add<S>(acc[w], unit_sum<T, 1>(one));
+      }
+    }
+  } else {
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+      const u64 r = r0 + q + (u64)w * tpr;
+      if (r < d.m) {
+        for (u64 j = c0 + g; j < c1; j += G) {
+          T in[K][1], v[1];
+          load_elem<T, EV>(d.f, j * d.m + r, in);
+          EV::template eval<T, 1>(in, d.f, v);
+          acc[w] = sum_add<S>(acc[w], unit_sum<T, 1>(v));
+        }
+      }
+    }
+  }
+  // combine column groups in g order
+#pragma unroll
+  for (int w = 0; w < W; ++w) red[threadIdx.x * W + w] = acc[w];
+  __syncthreads();
+  if (g == 0) {
+    for (uint32_t h = 1; h < G; ++h) {
+#pragma unroll
+      for (int w = 0; w < W; ++w) acc[w] = sum_add<S>(acc[w], red[(h * tpr + q) * W + w]);
+    }
+  }
+  // row index owned by (q, w)
+  auto row_of = [&](int w) -> u64 {
+    return vec_rows ? r0 + (u64)q * W + w : r0 + q + (u64)w * tpr;
+  };
+  if (d.nchunks == 1) {
+    if (g == 0) {
+#pragma unroll
+      for (int w = 0; w < W; ++w) {
+        const u64 r = row_of(w);
+        if (r < d.m) store_dim_value<T>(d, r, acc[w]);
+      }
+    }
+    return;
+  }
+  S* part = reinterpret_cast<S*>(d.part);
+  if (g == 0) {
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+      const u64 r = row_of(w);
+      if (r < d.m) part[cc * d.m + r] = acc[w];
+    }
+    __threadfence();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned t = atomicAdd(&d.tickets[rt], 1u);
+    last = (t == d.nchunks - 1);
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  if (g == 0) {
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+      const u64 r = row_of(w);
+      if (r < d.m) {
+        S tot = S(0);
+        for (uint32_t c = 0; c < d.nchunks; ++c) tot = sum_add<S>(tot, __ldcg(part + c * d.m + r));
+        store_dim_value<T>(d, r, tot);
+      }
+    }
+  }
+  if (threadIdx.x == 0) d.tickets[rt] = 0u;
+}
+
+}  // namespace coot

@@ -1,0 +1,43 @@
+// Internal interface between the host runtime (runtime.cu) and the per-type
+// kernel translation units (kernels_<type>.cu).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace coot {
+
+struct FusedArgs;
+struct DimArgs;
+
+struct FusedPlan {
+  int catalog;       // >= 0 catalog id, -1 interpreter
+  int interp_large;  // interpreter size class: 0 = <=4 operands / depth 4, 1 = <=8 / 8
+  int acc;           // AccKind
+  unsigned grid;
+};
+
+enum DimKernel { DIMK_DIM0_BLOCK = 0, DIMK_DIM0_WARP = 1, DIMK_DIM1 = 2 };
+
+struct DimPlan {
+  int kernel;        // DimKernel
+  int catalog;       // 0 = plain [L0] matrix, -1 interpreter
+  int interp_large;
+  unsigned grid;
+};
+
+template <class T>
+cudaError_t launch_fused_t(const FusedPlan& p, const FusedArgs& a, cudaStream_t s);
+template <class T>
+cudaError_t launch_dim_t(const DimPlan& p, const DimArgs& a, cudaStream_t s);
+template <class T>
+cudaError_t launch_combine_t(uint32_t kind, int acc, const void* parts, uint32_t nparts,
+                             unsigned long long len, void* result, unsigned grid, cudaStream_t s);
+template <class T>
+cudaError_t launch_empty_rec_t(int acc, void* out, cudaStream_t s);
+template <class T>
+cudaError_t launch_fill_t(uint32_t kind, unsigned long long seed, unsigned long long stream,
+                          unsigned long long start, unsigned long long count,
+                          unsigned long long n_rows, unsigned long long k, void* out,
+                          unsigned grid, cudaStream_t s);
+
+}  // namespace coot

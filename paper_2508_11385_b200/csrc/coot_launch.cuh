@@ -1,0 +1,235 @@
+// Kernel tables and launchers, instantiated once per element type in
+// kernels_<type>.cu (so the four type families compile in parallel).
+#pragma once
+#include "coot_dim.cuh"
+#include "coot_internal.h"
+
+namespace coot {
+
+typedef void (*FusedFn)(const FusedArgs);
+typedef void (*DimFn)(const DimArgs);
+
+// U (units per thread per iteration, issued together): more for few operands
+// so every thread keeps >= 32-64 bytes of loads in flight.
+constexpr int unroll_for(int k) { return k <= 1 ? 4 : 2; }
+
+template <class T, int ACC, int... Code>
+FusedFn catalog_kernel() {
+  typedef StaticProg<Code...> P;
+  if constexpr (P::template legal<T>()) {
+    return &fused_kernel<T, ACC, CatalogEval<P>, unroll_for(P::n_ops())>;
+  } else {
+    return nullptr;
+  }
+}
+
+template <class T, int ACC>
+FusedFn pick_fused_acc(int catalog, int interp_large) {
+  if constexpr (ACC == ACC_SUMSQ && !is_float<T>()) {
+    return nullptr;
+  } else {
+    switch (catalog) {
+#define COOT_X(id, ...) \
+  case id:              \
+    return catalog_kernel<T, ACC, __VA_ARGS__>();
+      COOT_CATALOG(COOT_X)
+#undef COOT_X
+      default:
+        break;
+    }
+    if (interp_large) return &fused_kernel<T, ACC, InterpEval<8, 8>, 1>;
+    return &fused_kernel<T, ACC, InterpEval<4, 4>, 1>;
+  }
+}
+
+template <class T>
+FusedFn pick_fused(const FusedPlan& p) {
+  switch (p.acc) {
+    case ACC_NONE: return pick_fused_acc<T, ACC_NONE>(p.catalog, p.interp_large);
+    case ACC_SUM: return pick_fused_acc<T, ACC_SUM>(p.catalog, p.interp_large);
+    case ACC_SUMSQ: return pick_fused_acc<T, ACC_SUMSQ>(p.catalog, p.interp_large);
+    case ACC_MINMAX: return pick_fused_acc<T, ACC_MINMAX>(p.catalog, p.interp_large);
+  }
+  return nullptr;
+}
+
+template <class T>
+cudaError_t launch_fused_t(const FusedPlan& p, const FusedArgs& a, cudaStream_t s) {
+  FusedFn k = pick_fused<T>(p);
+  if (!k) return cudaErrorInvalidDeviceFunction;
+  k<<<p.grid, kThreads, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+// Dimension sums: catalog [L0] (plain matrix) or the interpreter.
+template <class T, template <class, class> class KER>
+DimFn pick_dim_ev(const DimPlan& p) {
+  if (p.catalog == 0) return KER<T, CatalogEval<StaticProg<CL(0)>>>::run;
+  if (p.interp_large) return KER<T, InterpEval<8, 8>>::run;
+  return KER<T, InterpEval<4, 4>>::run;
+}
+
+template <class T, class EV>
+struct Dim0Block {
+  static constexpr DimFn run = &dim0_block_kernel<T, EV>;
+};
+template <class T, class EV>
+struct Dim0Warp {
+  static constexpr DimFn run = &dim0_warp_kernel<T, EV>;
+};
+template <class T, class EV>
+struct Dim1 {
+  static constexpr DimFn run = &dim1_kernel<T, EV>;
+};
+
+template <class T>
+cudaError_t launch_dim_t(const DimPlan& p, const DimArgs& a, cudaStream_t s) {
+  DimFn k = nullptr;
+  switch (p.kernel) {
+    case DIMK_DIM0_BLOCK: k = pick_dim_ev<T, Dim0Block>(p); break;
+    case DIMK_DIM0_WARP: k = pick_dim_ev<T, Dim0Warp>(p); break;
+    case DIMK_DIM1: k = pick_dim_ev<T, Dim1>(p); break;
+  }
+  if (!k) return cudaErrorInvalidDeviceFunction;
+  k<<<p.grid, kThreads, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+// ---- multi-GPU combine (K6) and partial bookkeeping -------------------------
+// Scalar partial records are merged strictly in part order 0..nparts-1.
+template <class T, int ACC>
+__global__ void combine_rec_kernel(const Rec* parts, uint32_t nparts, uint32_t kind,
+                                   void* result) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  Accum<T, ACC> acc;
+  acc.init();
+  for (uint32_t p = 0; p < nparts; ++p) {
+    Accum<T, ACC> o;
+    o.from_rec(parts[p]);
+    acc.merge(o);
+  }
+  write_final<T, ACC>(acc, kind, result);
+}
+
+// Vector partials (SUM_DIM*): result[i] = round(sum_p parts[p][i]), p in order.
+template <class T>
+__global__ void combine_vec_kernel(const typename SumT<T>::type* parts, uint32_t nparts, u64 len,
+                                   T* result) {
+  typedef typename SumT<T>::type S;
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < len;
+       i += (u64)gridDim.x * blockDim.x) {
+    S s = S(0);
+    for (uint32_t p = 0; p < nparts; ++p) s = sum_add<S>(s, parts[(u64)p * len + i]);
+    if constexpr (sizeof(T) == 4 && is_float<T>()) result[i] = __double2float_rn(s);
+    else result[i] = (T)s;
+  }
+}
+
+// Identity record for an empty shard (no elements => no kernel to publish it).
+template <class T, int ACC>
+__global__ void empty_rec_kernel(Rec* out) {
+  Accum<T, ACC> acc;
+  acc.init();
+  *out = acc.to_rec(0);
+}
+
+template <class T>
+cudaError_t launch_combine_t(uint32_t kind, int acc, const void* parts, uint32_t nparts, u64 len,
+                             void* result, unsigned grid, cudaStream_t s) {
+  if (kind == COOT_RED_SUM_DIM0 || kind == COOT_RED_SUM_DIM1) {
+    combine_vec_kernel<T><<<grid, kThreads, 0, s>>>(
+        reinterpret_cast<const typename SumT<T>::type*>(parts), nparts, len,
+        reinterpret_cast<T*>(result));
+    return cudaGetLastError();
+  }
+  const Rec* r = reinterpret_cast<const Rec*>(parts);
+  switch (acc) {
+    case ACC_SUM: combine_rec_kernel<T, ACC_SUM><<<1, 32, 0, s>>>(r, nparts, kind, result); break;
+    case ACC_SUMSQ:
+      if constexpr (is_float<T>()) {
+        combine_rec_kernel<T, ACC_SUMSQ><<<1, 32, 0, s>>>(r, nparts, kind, result);
+        break;
+      } else {
+        return cudaErrorInvalidValue;
+      }
+    case ACC_MINMAX:
+      combine_rec_kernel<T, ACC_MINMAX><<<1, 32, 0, s>>>(r, nparts, kind, result);
+      break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+template <class T>
+cudaError_t launch_empty_rec_t(int acc, void* out, cudaStream_t s) {
+  Rec* r = reinterpret_cast<Rec*>(out);
+  switch (acc) {
+    case ACC_SUM: empty_rec_kernel<T, ACC_SUM><<<1, 1, 0, s>>>(r); break;
+    case ACC_SUMSQ:
+      if constexpr (is_float<T>()) {
+        empty_rec_kernel<T, ACC_SUMSQ><<<1, 1, 0, s>>>(r);
+        break;
+      } else {
+        return cudaErrorInvalidValue;
+      }
+    case ACC_MINMAX: empty_rec_kernel<T, ACC_MINMAX><<<1, 1, 0, s>>>(r); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+// ---- synthetic input generator (harness) ---------
+__device__ __forceinline__ u64 splitmix_mix(u64 z) {
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+
+template <class T>
+__global__ void fill_kernel(uint32_t kind, u64 seed, u64 stream, u64 start, u64 count,
+                            u64 n_rows, u64 k, T* out) {
+  const u64 key = seed ^ (stream * 0xD1B54A32D192ED03ull);
+  for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < count;
+       i += (u64)gridDim.x * blockDim.x) {
+    const u64 g = start + i;
+    T v;
+    if (kind == 0) {
+      const u64 h = splitmix_mix(key + (g + 1) * 0x9E3779B97F4A7C15ull);
+      if constexpr (sizeof(T) == 4 && is_float<T>()) v = (float)(h >> 40) * 0x1p-24f;
+      else if constexpr (is_float<T>()) v = (double)(h >> 11) * 0x1p-53;
+      else if constexpr (sizeof(T) == 4) v = (T)(h >> 32);
+      else v = (T)h;
+    } else {
+      u64 iv = 0;
+      switch (kind) {
+        case 1: iv = 1; break;
+        case 2: iv = g; break;
+        case 3: iv = g % k; break;
+        case 4: iv = g / n_rows; break;
+        case 5: iv = g % n_rows; break;
+        default: iv = 0; break;
+      }
+      v = (T)iv;
+    }
+    out[i] = v;
+  }
+}
+
+template <class T>
+cudaError_t launch_fill_t(uint32_t kind, u64 seed, u64 stream, u64 start, u64 count, u64 n_rows,
+                          u64 k, void* out, unsigned grid, cudaStream_t s) {
+  fill_kernel<T><<<grid, kThreads, 0, s>>>(kind, seed, stream, start, count, n_rows ? n_rows : 1,
+                                           k ? k : 1, reinterpret_cast<T*>(out));
+  return cudaGetLastError();
+}
+
+#define COOT_INSTANTIATE(T)                                                                     \
+  template cudaError_t launch_fused_t<T>(const FusedPlan&, const FusedArgs&, cudaStream_t);   \
+  template cudaError_t launch_dim_t<T>(const DimPlan&, const DimArgs&, cudaStream_t);         \
+  template cudaError_t launch_combine_t<T>(uint32_t, int, const void*, uint32_t, u64, void*,  \
+                                           unsigned, cudaStream_t);                           \
+  template cudaError_t launch_empty_rec_t<T>(int, void*, cudaStream_t);                       \
+  template cudaError_t launch_fill_t<T>(uint32_t, u64, u64, u64, u64, u64, u64, void*,        \
+                                        unsigned, cudaStream_t);
+
+}  // namespace coot

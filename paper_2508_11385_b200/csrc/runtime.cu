@@ -1,0 +1,774 @@
+// libcoot host runtime: the C ABI of include/coot.h.
+//
+//   validate -> lower (catalog match / interpreter keys) -> geometry -> ONE launch
+//
+// Delayed evaluation (§3) happens above this layer (the Python
+// builder or any C caller assembles a coot_expr); at "assignment" the whole
+// expression is validated on the host and mapped to a single kernel — the
+// B200 analogue of "the minimal set of calls".  All validation is
+// host-only and happens before anything is enqueued.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+
+#include "coot_catalog.h"
+#include "coot_dim.cuh"
+#include "coot_internal.h"
+
+using coot::u64;
+
+struct coot_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  uint32_t flags = 0;
+  int sm_count = 0;
+  int cc_major = 0, cc_minor = 0;
+  int blocks_per_sm = 8;
+  coot::Rec* recs = nullptr;  // per-block records of the fused pass
+  unsigned max_grid = 0;
+  unsigned* ticket = nullptr;  // fused-pass arrival counter
+  void* dim_part = nullptr;
+  size_t dim_part_bytes = 0;
+  unsigned* dim_tickets = nullptr;
+  size_t dim_tickets_n = 0;
+  coot_stats_t stats{};
+  bool log = false;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+coot_status fail(coot_status s, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return s;
+}
+
+coot_status ok() { return COOT_OK; }
+
+coot_status cuda_fail(cudaError_t e, const char* what) {
+  return fail(COOT_ERR_DEVICE, "device: %s: %s (%s)", what, cudaGetErrorName(e),
+              cudaGetErrorString(e));
+}
+
+const char* op_name(int op) {
+  static const char* names[] = {"LOAD", "SCALAR", "NEG", "ABS", "SQUARE", "SQRT", "EXP",
+                                "LOG",  "ADD",    "SUB", "MUL", "DIV",    "MIN",  "MAX"};
+  return (op >= 0 && op < COOT_OP_COUNT_) ? names[op] : "?";
+}
+
+size_t elem_size(uint32_t elem) {
+  switch (elem) {
+    case COOT_F32: return 4;
+    case COOT_F64: return 8;
+    case COOT_U32: return 4;
+    case COOT_S64: return 8;
+  }
+  return 0;
+}
+
+bool is_float_elem(uint32_t e) { return e == COOT_F32 || e == COOT_F64; }
+bool is_unary(int op) { return op >= COOT_OP_NEG && op <= COOT_OP_LOG; }
+bool is_binary(int op) { return op >= COOT_OP_ADD && op <= COOT_OP_MAX; }
+
+int env_int(const char* name, int dflt) {
+  const char* v = getenv(name);
+  if (!v || !*v) return dflt;
+  return atoi(v);
+}
+
+// ---- validation -------------------------------------------------------------
+struct Shape {
+  int max_depth = 0;
+  uint32_t used_mask = 0;  // operands referenced by LOAD
+};
+
+coot_status validate_expr(const coot_expr* e, Shape* shape) {
+  if (!e) return fail(COOT_ERR_CONTRACT, "contract: expression descriptor is NULL");
+  if (e->abi_version != COOT_ABI_VERSION)
+    return fail(COOT_ERR_CONFIG, "configuration: descriptor abi_version %u, library %u",
+                e->abi_version, COOT_ABI_VERSION);
+  if (elem_size(e->elem) == 0)
+    return fail(COOT_ERR_CONTRACT, "contract: unknown element type %u", e->elem);
+  if (e->reserved != 0) return fail(COOT_ERR_CONTRACT, "contract: reserved field must be 0");
+  if (e->n_operands < 1 || e->n_operands > COOT_MAX_OPERANDS)
+    return fail(COOT_ERR_BOUNDS, "bounds: %u operands (allowed 1..%d)", e->n_operands,
+                COOT_MAX_OPERANDS);
+  if (e->n_scalars > COOT_MAX_SCALARS)
+    return fail(COOT_ERR_BOUNDS, "bounds: %u scalars (allowed 0..%d)", e->n_scalars,
+                COOT_MAX_SCALARS);
+  if (e->n_instr < 1 || e->n_instr > COOT_MAX_INSTR)
+    return fail(COOT_ERR_BOUNDS, "bounds: %u instructions (allowed 1..%d)", e->n_instr,
+                COOT_MAX_INSTR);
+  const u64 n = e->n_rows * e->n_cols;
+  if (e->n_cols != 0 && n / e->n_cols != e->n_rows)
+    return fail(COOT_ERR_BOUNDS, "bounds: %llux%llu overflows 64-bit element count",
+                (unsigned long long)e->n_rows, (unsigned long long)e->n_cols);
+  const size_t es = elem_size(e->elem);
+  for (uint32_t k = 0; k < e->n_operands; ++k) {
+    const coot_operand& o = e->operands[k];
+    if (o.ld != 0 && o.ld != o.n_rows)
+      return fail(COOT_ERR_CONTRACT,
+                  "contract: operand %u has leading dimension %llu != n_rows %llu "
+                  "(strided views are not supported by ABI v1)",
+                  k, (unsigned long long)o.ld, (unsigned long long)o.n_rows);
+    if (n > 0 && o.ptr == nullptr)
+      return fail(COOT_ERR_CONTRACT, "contract: operand %u is NULL with %llu elements", k,
+                  (unsigned long long)n);
+    if (reinterpret_cast<uintptr_t>(o.ptr) % es != 0)
+      return fail(COOT_ERR_CONTRACT, "contract: operand %u is not aligned to its %zu-byte element",
+                  k, es);
+  }
+  int sp = 0;
+  Shape sh;
+  for (uint32_t i = 0; i < e->n_instr; ++i) {
+    const int op = e->prog[i].op, arg = e->prog[i].arg;
+    if (op < 0 || op >= COOT_OP_COUNT_)
+      return fail(COOT_ERR_CONTRACT, "contract: unknown opcode %d @ instr %u", op, i);
+    if (!is_float_elem(e->elem) &&
+        (op == COOT_OP_SQRT || op == COOT_OP_EXP || op == COOT_OP_LOG || op == COOT_OP_DIV))
+      return fail(COOT_ERR_CONTRACT, "contract: %s is not defined for integer element types @ instr %u",
+                  op_name(op), i);
+    if (op == COOT_OP_LOAD) {
+      if ((uint32_t)arg >= e->n_operands)
+        return fail(COOT_ERR_CONTRACT, "contract: LOAD %d @ instr %u but only %u operands", arg, i,
+                    e->n_operands);
+      const coot_operand& o = e->operands[arg];
+      if (o.n_rows != e->n_rows || o.n_cols != e->n_cols)
+        return fail(COOT_ERR_CONFORM, "conformability: operand %d is %llux%llu, expression is %llux%llu (LOAD @ instr %u)",
+                    arg, (unsigned long long)o.n_rows, (unsigned long long)o.n_cols,
+                    (unsigned long long)e->n_rows, (unsigned long long)e->n_cols, i);
+      sh.used_mask |= 1u << arg;
+      ++sp;
+    } else if (op == COOT_OP_SCALAR) {
+      if ((uint32_t)arg >= e->n_scalars)
+        return fail(COOT_ERR_CONTRACT, "contract: SCALAR %d @ instr %u but only %u scalars", arg, i,
+                    e->n_scalars);
+      ++sp;
+    } else if (is_unary(op)) {
+      if (arg != 0) return fail(COOT_ERR_CONTRACT, "contract: %s takes no argument @ instr %u", op_name(op), i);
+      if (sp < 1) return fail(COOT_ERR_CONTRACT, "contract: stack underflow at %s @ instr %u", op_name(op), i);
+    } else {
+      if (arg != 0) return fail(COOT_ERR_CONTRACT, "contract: %s takes no argument @ instr %u", op_name(op), i);
+      if (sp < 2) return fail(COOT_ERR_CONTRACT, "contract: stack underflow at %s @ instr %u", op_name(op), i);
+      --sp;
+    }
+    if (sp > COOT_MAX_STACK)
+      return fail(COOT_ERR_BOUNDS, "bounds: stack depth %d exceeds %d @ instr %u", sp, COOT_MAX_STACK, i);
+    sh.max_depth = std::max(sh.max_depth, sp);
+  }
+  if (sp != 1)
+    return fail(COOT_ERR_CONTRACT, "contract: program leaves %d values on the stack (expected 1)", sp);
+  if (sh.used_mask == 0) return fail(COOT_ERR_CONTRACT, "contract: program reads no operand");
+  // Unreferenced operands are allowed but their dims must still conform.
+  for (uint32_t k = 0; k < e->n_operands; ++k) {
+    const coot_operand& o = e->operands[k];
+    if (o.n_rows != e->n_rows || o.n_cols != e->n_cols)
+      return fail(COOT_ERR_CONFORM, "conformability: operand %u is %llux%llu, expression is %llux%llu",
+                  k, (unsigned long long)o.n_rows, (unsigned long long)o.n_cols,
+                  (unsigned long long)e->n_rows, (unsigned long long)e->n_cols);
+  }
+  if (shape) *shape = sh;
+  return ok();
+}
+
+bool ranges_overlap(uintptr_t a, size_t na, uintptr_t b, size_t nb) {
+  if (na == 0 || nb == 0) return false;
+  return a < b + nb && b < a + na;
+}
+
+// out may equal an operand exactly (B += 3*A); any other overlap is an error.
+coot_status check_out_alias(const coot_expr* e, const void* out, size_t bytes) {
+  if (!out) return ok();
+  const uintptr_t o = reinterpret_cast<uintptr_t>(out);
+  for (uint32_t k = 0; k < e->n_operands; ++k) {
+    const uintptr_t p = reinterpret_cast<uintptr_t>(e->operands[k].ptr);
+    if (p == o) continue;
+    if (ranges_overlap(o, bytes, p, bytes))
+      return fail(COOT_ERR_CONTRACT, "contract: out partially overlaps operand %u (only exact aliasing is allowed)", k);
+  }
+  return ok();
+}
+
+coot_status check_result_alias(const coot_expr* e, const void* result, size_t rbytes,
+                               const void* out, size_t bytes) {
+  const uintptr_t r = reinterpret_cast<uintptr_t>(result);
+  for (uint32_t k = 0; k < e->n_operands; ++k)
+    if (ranges_overlap(r, rbytes, reinterpret_cast<uintptr_t>(e->operands[k].ptr), bytes))
+      return fail(COOT_ERR_CONTRACT, "contract: result overlaps operand %u", k);
+  if (out && ranges_overlap(r, rbytes, reinterpret_cast<uintptr_t>(out), bytes))
+    return fail(COOT_ERR_CONTRACT, "contract: result overlaps out");
+  return ok();
+}
+
+// ---- lowering ---------------------------------------------------------------
+struct CatalogEntry {
+  int id;
+  int n;
+  int code[COOT_MAX_INSTR];
+};
+
+template <int... C>
+constexpr int count_codes() {
+  return (int)sizeof...(C);
+}
+#define COOT_X(id, ...) {id, count_codes<__VA_ARGS__>(), {__VA_ARGS__}},
+const CatalogEntry kCatalog[] = {COOT_CATALOG(COOT_X)};
+#undef COOT_X
+
+int match_catalog(const coot_expr* e) {
+  for (const CatalogEntry& c : kCatalog) {
+    if ((uint32_t)c.n != e->n_instr) continue;
+    bool same = true;
+    for (int i = 0; i < c.n && same; ++i)
+      same = c.code[i] == COOT_I(e->prog[i].op, e->prog[i].arg);
+    if (same) return c.id;
+  }
+  return -1;
+}
+
+// Pack everything the evaluators need into the kernel arguments.
+void fill_program(const coot_expr* e, coot::FusedArgs* a) {
+  for (uint32_t k = 0; k < COOT_MAX_OPERANDS; ++k)
+    a->in[k] = k < e->n_operands ? e->operands[k].ptr : nullptr;
+  for (uint32_t s = 0; s < COOT_MAX_SCALARS; ++s)
+    a->scalars[s] = s < e->n_scalars ? e->scalars[s].bits : 0;
+  a->n_operands = e->n_operands;
+  a->n_instr = e->n_instr;
+  int sp = 0;
+  for (uint32_t i = 0; i < e->n_instr; ++i) {
+    const int op = e->prog[i].op, arg = e->prog[i].arg;
+    a->key[i] = (uint16_t)COOT_KEY(op, sp, op == COOT_OP_LOAD ? arg : 0);
+    a->arg[i] = (uint8_t)arg;
+    if (op == COOT_OP_LOAD || op == COOT_OP_SCALAR) ++sp;
+    else if (is_binary(op)) --sp;
+  }
+}
+
+int acc_for_kind(uint32_t kind) {
+  switch (kind) {
+    case COOT_RED_ACCU: return coot::ACC_SUM;
+    case COOT_RED_NORM2: return coot::ACC_SUMSQ;
+    case COOT_RED_MIN:
+    case COOT_RED_MAX:
+    case COOT_RED_MINMAX: return coot::ACC_MINMAX;
+  }
+  return -1;
+}
+
+size_t result_bytes(uint32_t kind, size_t es, u64 m, u64 n) {
+  switch (kind) {
+    case COOT_RED_MINMAX: return 2 * es;
+    case COOT_RED_SUM_DIM0: return n * es;
+    case COOT_RED_SUM_DIM1: return m * es;
+  }
+  return es;
+}
+
+cudaError_t dispatch_fused(uint32_t elem, const coot::FusedPlan& p, const coot::FusedArgs& a,
+                           cudaStream_t s) {
+  switch (elem) {
+    case COOT_F32: return coot::launch_fused_t<float>(p, a, s);
+    case COOT_F64: return coot::launch_fused_t<double>(p, a, s);
+    case COOT_U32: return coot::launch_fused_t<uint32_t>(p, a, s);
+    case COOT_S64: return coot::launch_fused_t<coot::s64>(p, a, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t dispatch_dim(uint32_t elem, const coot::DimPlan& p, const coot::DimArgs& a,
+                         cudaStream_t s) {
+  switch (elem) {
+    case COOT_F32: return coot::launch_dim_t<float>(p, a, s);
+    case COOT_F64: return coot::launch_dim_t<double>(p, a, s);
+    case COOT_U32: return coot::launch_dim_t<uint32_t>(p, a, s);
+    case COOT_S64: return coot::launch_dim_t<coot::s64>(p, a, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
+coot_status bind_device(coot_ctx* ctx) {
+  int cur = -1;
+  cudaError_t e = cudaGetDevice(&cur);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaGetDevice");
+  if (cur != ctx->device) {
+    e = cudaSetDevice(ctx->device);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+  }
+  return ok();
+}
+
+coot_status grow_dim_scratch(coot_ctx* ctx, size_t part_bytes, size_t ntickets) {
+  if (part_bytes <= ctx->dim_part_bytes && ntickets <= ctx->dim_tickets_n) return ok();
+  cudaError_t e = cudaStreamSynchronize(ctx->stream);  // old buffers may be in use
+  if (e != cudaSuccess) return cuda_fail(e, "cudaStreamSynchronize");
+  if (part_bytes > ctx->dim_part_bytes) {
+    cudaFree(ctx->dim_part);
+    ctx->dim_part = nullptr;
+    ctx->dim_part_bytes = 0;
+    e = cudaMalloc(&ctx->dim_part, part_bytes);
+    if (e != cudaSuccess)
+      return fail(COOT_ERR_RESOURCE, "resource: cannot allocate %zu bytes of reduction scratch", part_bytes);
+    ctx->dim_part_bytes = part_bytes;
+  }
+  if (ntickets > ctx->dim_tickets_n) {
+    cudaFree(ctx->dim_tickets);
+    ctx->dim_tickets = nullptr;
+    ctx->dim_tickets_n = 0;
+    e = cudaMalloc(&ctx->dim_tickets, ntickets * sizeof(unsigned));
+    if (e != cudaSuccess)
+      return fail(COOT_ERR_RESOURCE, "resource: cannot allocate %zu ticket counters", ntickets);
+    e = cudaMemset(ctx->dim_tickets, 0, ntickets * sizeof(unsigned));
+    if (e != cudaSuccess) return cuda_fail(e, "cudaMemset");
+    ctx->dim_tickets_n = ntickets;
+  }
+  return ok();
+}
+
+u64 ceil_div(u64 a, u64 b) { return (a + b - 1) / b; }
+
+u64 alg_bytes(const coot_expr* e, const Shape& sh, bool store) {
+  const u64 n = e->n_rows * e->n_cols;
+  const u64 k = (u64)__builtin_popcount(sh.used_mask) + (store ? 1 : 0);
+  return n * elem_size(e->elem) * k;
+}
+
+// The fused pass (eval / full reductions).
+coot_status run_fused(coot_ctx* ctx, const coot_expr* e, const Shape& sh, int acc, uint32_t kind,
+                      void* result, uint32_t final_mode, void* out) {
+  const size_t es = elem_size(e->elem);
+  const u64 n = e->n_rows * e->n_cols;
+  const u64 W = 16 / es;
+  coot::FusedArgs a;
+  memset(&a, 0, sizeof a);
+  fill_program(e, &a);
+  a.out = out;
+  a.n = n;
+  // 16-byte unit path iff every accessed array has the same misalignment.
+  const uintptr_t mis = reinterpret_cast<uintptr_t>(e->operands[0].ptr) & 15;
+  bool vec_ok = true;
+  for (uint32_t k = 0; k < e->n_operands; ++k)
+    vec_ok = vec_ok && ((reinterpret_cast<uintptr_t>(e->operands[k].ptr) & 15) == mis);
+  if (out) vec_ok = vec_ok && ((reinterpret_cast<uintptr_t>(out) & 15) == mis);
+  if (vec_ok) {
+    u64 head = mis ? (16 - mis) / es : 0;
+    if (head > n) head = n;
+    a.head = head;
+    a.nunits = (n - head) / W;
+    a.tail_begin = head + a.nunits * W;
+  } else {
+    a.head = n;
+    a.nunits = 0;
+    a.tail_begin = n;
+  }
+  const u64 work = std::max<u64>(std::max<u64>(a.nunits, a.head), n - a.tail_begin);
+  u64 grid = std::max<u64>(1, ceil_div(work, coot::kThreads));
+  grid = std::min<u64>(grid, (u64)ctx->sm_count * ctx->blocks_per_sm);
+  a.partials = ctx->recs;
+  a.ticket = ctx->ticket;
+  a.result = result;
+  a.count = n;
+  a.final_mode = final_mode;
+  a.kind = kind;
+
+  coot::FusedPlan p;
+  p.catalog = (ctx->flags & COOT_INIT_FORCE_INTERP) ? -1 : match_catalog(e);
+  p.interp_large = (e->n_operands > 4 || sh.max_depth > 4) ? 1 : 0;
+  p.acc = acc;
+  p.grid = (unsigned)grid;
+  if (ctx->log)
+    fprintf(stderr, "[coot] fused elem=%u n=%llu path=%d%s acc=%d grid=%u head=%llu units=%llu\n",
+            e->elem, (unsigned long long)n, p.catalog, p.catalog < 0 ? (p.interp_large ? "(interp8)" : "(interp4)") : "",
+            acc, p.grid, (unsigned long long)a.head, (unsigned long long)a.nunits);
+  cudaError_t ce = dispatch_fused(e->elem, p, a, ctx->stream);
+  if (ce != cudaSuccess) return cuda_fail(ce, "fused kernel launch");
+  ctx->stats.launches++;
+  ctx->stats.last_path = p.catalog;
+  ctx->stats.last_grid = p.grid;
+  ctx->stats.last_alg_bytes = alg_bytes(e, sh, out != nullptr);
+  return ok();
+}
+
+// sum(X, 0) / sum(X, 1).
+coot_status run_dim(coot_ctx* ctx, const coot_expr* e, const Shape& sh, uint32_t kind,
+                    void* result, uint32_t final_mode) {
+  const size_t es = elem_size(e->elem);
+  const u64 m = e->n_rows, n = e->n_cols;
+  const u64 W = 16 / es;
+  const size_t sbytes = 8;  // f64 / u64 partial words
+  const u64 nout = kind == COOT_RED_SUM_DIM0 ? n : m;
+  const size_t obytes = final_mode == coot::FINAL_PARTIAL ? sbytes : es;
+  if (m == 0 || n == 0) {
+    if (nout) {
+      cudaError_t ce = cudaMemsetAsync(result, 0, nout * obytes, ctx->stream);
+      if (ce != cudaSuccess) return cuda_fail(ce, "cudaMemsetAsync");
+    }
+    return ok();
+  }
+  coot::DimArgs d;
+  memset(&d, 0, sizeof d);
+  fill_program(e, &d.f);
+  d.m = m;
+  d.n = n;
+  d.result = result;
+  d.final_mode = final_mode;
+  const uintptr_t mis = reinterpret_cast<uintptr_t>(e->operands[0].ptr) & 15;
+  bool same = true;
+  for (uint32_t k = 0; k < e->n_operands; ++k)
+    same = same && ((reinterpret_cast<uintptr_t>(e->operands[k].ptr) & 15) == mis);
+  const bool col_aligned = ((m * es) % 16) == 0;
+  const u64 target = (u64)ctx->sm_count * ctx->blocks_per_sm;
+  coot::DimPlan p;
+  p.catalog = ((ctx->flags & COOT_INIT_FORCE_INTERP) == 0 && e->n_instr == 1) ? 0 : -1;
+  p.interp_large = (e->n_operands > 4 || sh.max_depth > 4) ? 1 : 0;
+  size_t part_bytes = 0, ntickets = 0;
+  if (kind == COOT_RED_SUM_DIM0) {
+    d.vec_ok = (same && col_aligned) ? 1 : 0;
+    if (m >= 2048) {
+      p.kernel = coot::DIMK_DIM0_BLOCK;
+      u64 S = std::max<u64>(1, ceil_div(target, n));
+      S = std::min<u64>(S, std::max<u64>(1, m / 2048));
+      u64 L = ceil_div(m, S);
+      L = ceil_div(L, 4 * W) * 4 * W;
+      S = ceil_div(m, L);
+      d.seg_len = L;
+      d.nseg = (uint32_t)S;
+      p.grid = (unsigned)std::min<u64>(n * S, target);
+      if (S > 1) {
+        part_bytes = n * S * sbytes;
+        ntickets = n;
+      }
+    } else {
+      p.kernel = coot::DIMK_DIM0_WARP;
+      d.seg_len = m;
+      d.nseg = 1;
+      p.grid = (unsigned)std::min<u64>(ceil_div(n * 32, coot::kThreads), target);
+    }
+  } else {
+    p.kernel = coot::DIMK_DIM1;
+    d.vec_ok = (same && mis == 0 && col_aligned) ? 1 : 0;
+    uint32_t tpr = 32;
+    while (tpr < (uint32_t)coot::kThreads && (u64)tpr * W < m) tpr *= 2;
+    const u64 G = coot::kThreads / tpr;
+    const u64 R = (u64)tpr * W;
+    const u64 nrt = ceil_div(m, R);
+    u64 nchunks = std::max<u64>(1, ceil_div(target, nrt));
+    nchunks = std::min<u64>(nchunks, std::max<u64>(1, n / (8 * G)));
+    const u64 ccols = ceil_div(n, nchunks);
+    nchunks = ceil_div(n, ccols);
+    d.tpr = tpr;
+    d.nrt = (uint32_t)nrt;
+    d.ccols = ccols;
+    d.nchunks = (uint32_t)nchunks;
+    p.grid = (unsigned)(nrt * nchunks);
+    if (nchunks > 1) {
+      part_bytes = nchunks * m * sbytes;
+      ntickets = nrt;
+    }
+  }
+  coot_status st = grow_dim_scratch(ctx, part_bytes, ntickets);
+  if (st != COOT_OK) return st;
+  d.part = ctx->dim_part;
+  d.tickets = ctx->dim_tickets;
+  if (ctx->log)
+    fprintf(stderr, "[coot] dim%d elem=%u %llux%llu kernel=%d grid=%u nseg=%u nchunks=%u tpr=%u vec=%u\n",
+            kind == COOT_RED_SUM_DIM0 ? 0 : 1, e->elem, (unsigned long long)m, (unsigned long long)n,
+            p.kernel, p.grid, d.nseg, d.nchunks, d.tpr, d.vec_ok);
+  cudaError_t ce = dispatch_dim(e->elem, p, d, ctx->stream);
+  if (ce != cudaSuccess) return cuda_fail(ce, "dim kernel launch");
+  ctx->stats.launches++;
+  ctx->stats.last_path = -2;
+  ctx->stats.last_grid = p.grid;
+  ctx->stats.last_alg_bytes = alg_bytes(e, sh, false) + nout * es;
+  return ok();
+}
+
+coot_status check_ctx(const coot_ctx* ctx) {
+  if (!ctx) return fail(COOT_ERR_CONFIG, "configuration: ctx is NULL");
+  return ok();
+}
+
+coot_status reduce_common(coot_ctx* ctx, const coot_expr* e, uint32_t kind, void* result,
+                          void* out, uint32_t final_mode) {
+  coot_status st = check_ctx(ctx);
+  if (st != COOT_OK) return st;
+  Shape sh;
+  st = validate_expr(e, &sh);
+  if (st != COOT_OK) return st;
+  if (kind >= COOT_RED_COUNT_) return fail(COOT_ERR_CONTRACT, "contract: unknown reduction kind %u", kind);
+  if (!result) return fail(COOT_ERR_CONTRACT, "contract: result is NULL");
+  const size_t es = elem_size(e->elem);
+  const u64 n = e->n_rows * e->n_cols;
+  if (kind == COOT_RED_NORM2 && !is_float_elem(e->elem))
+    return fail(COOT_ERR_CONTRACT, "contract: NORM2 is defined for f32/f64 only");
+  const bool dim = kind == COOT_RED_SUM_DIM0 || kind == COOT_RED_SUM_DIM1;
+  if (dim && out)
+    return fail(COOT_ERR_CONTRACT, "contract: out_or_null must be NULL for SUM_DIM reductions");
+  if (final_mode == coot::FINAL_ROUND && n == 0 &&
+      (kind == COOT_RED_MIN || kind == COOT_RED_MAX || kind == COOT_RED_MINMAX))
+    return fail(COOT_ERR_CONTRACT, "contract: min/max of an empty expression");
+  st = check_out_alias(e, out, n * es);
+  if (st != COOT_OK) return st;
+  size_t rbytes = result_bytes(kind, es, e->n_rows, e->n_cols);
+  if (final_mode == coot::FINAL_PARTIAL)
+    rbytes = dim ? (kind == COOT_RED_SUM_DIM0 ? e->n_cols : e->n_rows) * 8 : COOT_PARTIAL_BYTES;
+  st = check_result_alias(e, result, rbytes, out, n * es);
+  if (st != COOT_OK) return st;
+  st = bind_device(ctx);
+  if (st != COOT_OK) return st;
+  if (dim) return run_dim(ctx, e, sh, kind, result, final_mode);
+  const int acc = acc_for_kind(kind);
+  if (n == 0) {
+    if (final_mode == coot::FINAL_PARTIAL) {
+      cudaError_t ce;
+      switch (e->elem) {
+        case COOT_F32: ce = coot::launch_empty_rec_t<float>(acc, result, ctx->stream); break;
+        case COOT_F64: ce = coot::launch_empty_rec_t<double>(acc, result, ctx->stream); break;
+        case COOT_U32: ce = coot::launch_empty_rec_t<uint32_t>(acc, result, ctx->stream); break;
+        default: ce = coot::launch_empty_rec_t<coot::s64>(acc, result, ctx->stream); break;
+      }
+      if (ce != cudaSuccess) return cuda_fail(ce, "empty record launch");
+      ctx->stats.launches++;
+      return ok();
+    }
+    cudaError_t ce = cudaMemsetAsync(result, 0, es, ctx->stream);  // ACCU / NORM2 of empty = 0
+    if (ce != cudaSuccess) return cuda_fail(ce, "cudaMemsetAsync");
+    return ok();
+  }
+  return run_fused(ctx, e, sh, acc, kind, result, final_mode, out);
+}
+
+}  // namespace
+
+// ============================================================================
+extern "C" {
+
+uint32_t coot_abi_version(void) { return COOT_ABI_VERSION; }
+
+const char* coot_last_error(void) { return g_err.c_str(); }
+
+const char* coot_status_string(coot_status s) {
+  switch (s) {
+    case COOT_OK: return "ok";
+    case COOT_ERR_CONFIG: return "configuration";
+    case COOT_ERR_CONFORM: return "conformability";
+    case COOT_ERR_BOUNDS: return "bounds";
+    case COOT_ERR_RESOURCE: return "resource";
+    case COOT_ERR_CONTRACT: return "contract";
+    case COOT_ERR_DEVICE: return "device";
+  }
+  return "unknown";
+}
+
+coot_status coot_validate(const coot_expr* e) { return validate_expr(e, nullptr); }
+
+coot_status coot_init(coot_ctx** out, int device, void* cuda_stream, uint32_t flags) {
+  if (!out) return fail(COOT_ERR_CONFIG, "configuration: out is NULL");
+  *out = nullptr;
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess || ndev == 0)
+    return fail(COOT_ERR_CONFIG, "configuration: no CUDA device (%s)", cudaGetErrorString(e));
+  if (device < 0 || device >= ndev)
+    return fail(COOT_ERR_CONFIG, "configuration: device %d out of range (0..%d)", device, ndev - 1);
+  e = cudaSetDevice(device);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+  coot_ctx* ctx = new coot_ctx();
+  ctx->device = device;
+  ctx->stream = reinterpret_cast<cudaStream_t>(cuda_stream);
+  ctx->flags = flags;
+  if (env_int("COOT_FORCE_INTERP", 0)) ctx->flags |= COOT_INIT_FORCE_INTERP;
+  ctx->log = env_int("COOT_LOG", 0) != 0;
+  cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, device);
+  cudaDeviceGetAttribute(&ctx->cc_major, cudaDevAttrComputeCapabilityMajor, device);
+  cudaDeviceGetAttribute(&ctx->cc_minor, cudaDevAttrComputeCapabilityMinor, device);
+  if (ctx->cc_major != 10) {
+    int maj = ctx->cc_major, min = ctx->cc_minor;
+    delete ctx;
+    return fail(COOT_ERR_CONFIG, "configuration: device %d is sm_%d%d; libcoot is built for sm_100a (compute capability 10.x)",
+                device, maj, min);
+  }
+  ctx->blocks_per_sm = std::max(1, std::min(32, env_int("COOT_BLOCKS_PER_SM", 8)));
+  ctx->max_grid = (unsigned)ctx->sm_count * 32u;
+  e = cudaMalloc(&ctx->recs, sizeof(coot::Rec) * ctx->max_grid);
+  if (e == cudaSuccess) e = cudaMalloc(&ctx->ticket, 64 * sizeof(unsigned));
+  if (e == cudaSuccess) e = cudaMemset(ctx->ticket, 0, 64 * sizeof(unsigned));
+  if (e != cudaSuccess) {
+    cudaFree(ctx->recs);
+    cudaFree(ctx->ticket);
+    delete ctx;
+    return fail(COOT_ERR_RESOURCE, "resource: cannot allocate reduction scratch (%s)", cudaGetErrorString(e));
+  }
+  ctx->stats.sm_count = ctx->sm_count;
+  ctx->stats.last_path = -3;
+  if (flags & COOT_INIT_PRINT_INFO) {
+    cudaDeviceProp prop;
+    cudaGetDeviceProperties(&prop, device);
+    fprintf(stderr, "[coot] device %d: %s, sm_%d%d, %d SMs, %.1f GB, L2 %d MB, libcoot ABI %u\n",
+            device, prop.name, ctx->cc_major, ctx->cc_minor, ctx->sm_count,
+            prop.totalGlobalMem / 1e9, prop.l2CacheSize >> 20, COOT_ABI_VERSION);
+  }
+  *out = ctx;
+  return ok();
+}
+
+coot_status coot_destroy(coot_ctx* ctx) {
+  if (!ctx) return ok();
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  cudaFree(ctx->recs);
+  cudaFree(ctx->ticket);
+  cudaFree(ctx->dim_part);
+  cudaFree(ctx->dim_tickets);
+  delete ctx;
+  return ok();
+}
+
+coot_status coot_set_stream(coot_ctx* ctx, void* cuda_stream) {
+  coot_status st = check_ctx(ctx);
+  if (st != COOT_OK) return st;
+  if (reinterpret_cast<cudaStream_t>(cuda_stream) != ctx->stream) {
+    // the ticket counters are stream-ordered: drain the old stream first
+    cudaError_t e = cudaStreamSynchronize(ctx->stream);
+    if (e != cudaSuccess) return cuda_fail(e, "cudaStreamSynchronize");
+    ctx->stream = reinterpret_cast<cudaStream_t>(cuda_stream);
+  }
+  return ok();
+}
+
+coot_status coot_eval(coot_ctx* ctx, const coot_expr* e, void* out) {
+  coot_status st = check_ctx(ctx);
+  if (st != COOT_OK) return st;
+  Shape sh;
+  st = validate_expr(e, &sh);
+  if (st != COOT_OK) return st;
+  const u64 n = e->n_rows * e->n_cols;
+  if (n == 0) return ok();  // zero launches for an empty expression
+  if (!out) return fail(COOT_ERR_CONTRACT, "contract: out is NULL");
+  st = check_out_alias(e, out, n * elem_size(e->elem));
+  if (st != COOT_OK) return st;
+  if (reinterpret_cast<uintptr_t>(out) % elem_size(e->elem))
+    return fail(COOT_ERR_CONTRACT, "contract: out is not aligned to its element size");
+  st = bind_device(ctx);
+  if (st != COOT_OK) return st;
+  return run_fused(ctx, e, sh, coot::ACC_NONE, COOT_RED_ACCU, nullptr, coot::FINAL_ROUND, out);
+}
+
+coot_status coot_reduce(coot_ctx* ctx, const coot_expr* e, uint32_t kind, void* result,
+                        void* out_or_null) {
+  return reduce_common(ctx, e, kind, result, out_or_null, coot::FINAL_ROUND);
+}
+
+coot_status coot_reduce_partial(coot_ctx* ctx, const coot_expr* e, uint32_t kind, void* partial,
+                                void* out_or_null) {
+  return reduce_common(ctx, e, kind, partial, out_or_null, coot::FINAL_PARTIAL);
+}
+
+coot_status coot_partial_bytes(uint32_t kind, uint64_t len, uint64_t* bytes) {
+  if (!bytes) return fail(COOT_ERR_CONTRACT, "contract: bytes is NULL");
+  if (kind >= COOT_RED_COUNT_) return fail(COOT_ERR_CONTRACT, "contract: unknown reduction kind %u", kind);
+  *bytes = (kind == COOT_RED_SUM_DIM0 || kind == COOT_RED_SUM_DIM1) ? len * 8 : COOT_PARTIAL_BYTES;
+  return ok();
+}
+
+coot_status coot_combine(coot_ctx* ctx, uint32_t elem, uint32_t kind, const void* partials,
+                         uint32_t nparts, uint64_t len, void* result) {
+  coot_status st = check_ctx(ctx);
+  if (st != COOT_OK) return st;
+  if (elem_size(elem) == 0) return fail(COOT_ERR_CONTRACT, "contract: unknown element type %u", elem);
+  if (kind >= COOT_RED_COUNT_) return fail(COOT_ERR_CONTRACT, "contract: unknown reduction kind %u", kind);
+  if (kind == COOT_RED_NORM2 && !is_float_elem(elem))
+    return fail(COOT_ERR_CONTRACT, "contract: NORM2 is defined for f32/f64 only");
+  if (nparts == 0) return fail(COOT_ERR_CONTRACT, "contract: combine of zero partials");
+  if (!partials || !result) return fail(COOT_ERR_CONTRACT, "contract: NULL partials/result");
+  const bool dim = kind == COOT_RED_SUM_DIM0 || kind == COOT_RED_SUM_DIM1;
+  if (dim && len == 0) return ok();
+  st = bind_device(ctx);
+  if (st != COOT_OK) return st;
+  const unsigned grid = (unsigned)std::max<u64>(
+      1, std::min<u64>(ceil_div(dim ? len : 1, coot::kThreads), (u64)ctx->sm_count * 8));
+  const int acc = dim ? coot::ACC_SUM : acc_for_kind(kind);
+  cudaError_t ce;
+  switch (elem) {
+    case COOT_F32: ce = coot::launch_combine_t<float>(kind, acc, partials, nparts, len, result, grid, ctx->stream); break;
+    case COOT_F64: ce = coot::launch_combine_t<double>(kind, acc, partials, nparts, len, result, grid, ctx->stream); break;
+    case COOT_U32: ce = coot::launch_combine_t<uint32_t>(kind, acc, partials, nparts, len, result, grid, ctx->stream); break;
+    default: ce = coot::launch_combine_t<coot::s64>(kind, acc, partials, nparts, len, result, grid, ctx->stream); break;
+  }
+  if (ce != cudaSuccess) return cuda_fail(ce, "combine kernel launch");
+  ctx->stats.launches++;
+  ctx->stats.last_path = -3;
+  ctx->stats.last_grid = grid;
+  return ok();
+}
+
+coot_status coot_shard_range(uint64_t n, uint32_t rank, uint32_t nranks, uint64_t align,
+                             uint64_t* begin, uint64_t* end) {
+  if (!begin || !end) return fail(COOT_ERR_CONTRACT, "contract: NULL begin/end");
+  if (nranks == 0 || rank >= nranks)
+    return fail(COOT_ERR_CONFIG, "configuration: rank %u of %u", rank, nranks);
+  if (align == 0) align = 1;
+  auto cut = [&](uint64_t r) -> uint64_t {
+    if (r == 0) return 0;
+    if (r >= nranks) return n;
+    const unsigned __int128 c = (unsigned __int128)r * n / nranks;
+    return (uint64_t)c / align * align;
+  };
+  *begin = cut(rank);
+  *end = cut(rank + 1);
+  return ok();
+}
+
+coot_status coot_fill(coot_ctx* ctx, uint32_t elem, uint32_t fill_kind, uint64_t seed,
+                      uint64_t stream, uint64_t start, uint64_t count, uint64_t n_rows,
+                      uint64_t k, void* out) {
+  coot_status st = check_ctx(ctx);
+  if (st != COOT_OK) return st;
+  if (elem_size(elem) == 0) return fail(COOT_ERR_CONTRACT, "contract: unknown element type %u", elem);
+  if (fill_kind > 6) return fail(COOT_ERR_CONTRACT, "contract: unknown fill kind %u", fill_kind);
+  if (count == 0) return ok();
+  if (!out) return fail(COOT_ERR_CONTRACT, "contract: out is NULL");
+  st = bind_device(ctx);
+  if (st != COOT_OK) return st;
+  const unsigned grid = (unsigned)std::min<u64>(ceil_div(count, coot::kThreads), (u64)ctx->sm_count * 8);
+  cudaError_t ce;
+  switch (elem) {
+    case COOT_F32: ce = coot::launch_fill_t<float>(fill_kind, seed, stream, start, count, n_rows, k, out, grid, ctx->stream); break;
+    case COOT_F64: ce = coot::launch_fill_t<double>(fill_kind, seed, stream, start, count, n_rows, k, out, grid, ctx->stream); break;
+    case COOT_U32: ce = coot::launch_fill_t<uint32_t>(fill_kind, seed, stream, start, count, n_rows, k, out, grid, ctx->stream); break;
+    default: ce = coot::launch_fill_t<coot::s64>(fill_kind, seed, stream, start, count, n_rows, k, out, grid, ctx->stream); break;
+  }
+  if (ce != cudaSuccess) return cuda_fail(ce, "fill kernel launch");
+  ctx->stats.launches++;
+  ctx->stats.last_path = -3;
+  ctx->stats.last_grid = grid;
+  return ok();
+}
+
+coot_status coot_sync(coot_ctx* ctx) {
+  coot_status st = check_ctx(ctx);
+  if (st != COOT_OK) return st;
+  cudaError_t e = cudaStreamSynchronize(ctx->stream);
+  if (e != cudaSuccess) return cuda_fail(e, "asynchronous fault");
+  return ok();
+}
+
+coot_status coot_stats(const coot_ctx* ctx, coot_stats_t* out) {
+  coot_status st = check_ctx(ctx);
+  if (st != COOT_OK) return st;
+  if (!out) return fail(COOT_ERR_CONTRACT, "contract: out is NULL");
+  *out = ctx->stats;
+  return ok();
+}
+
+}  // extern "C"

@@ -1,0 +1,98 @@
+"""Multi-GPU sharding of the fused path (one process per GPU).
+
+Partitioning (reading R17): a long Col / Mat is split into contiguous blocks
+of the global linear index — for a column-major Mat, blocks of whole columns —
+with ``coot_shard_range``.  Each rank evaluates its block with ONE fused
+kernel that writes an UNROUNDED partial (``coot_reduce_partial``: a 32-byte
+record, or an f64/u64 vector for sum(X,1) over column shards).  The only
+exchange step of the method is the all-gather of those partials
+(torch.distributed, NCCL over NVLink/NVSwitch on B200; gloo on CPU / for
+host-staged tests), followed by ``coot_combine``: a kernel that merges the
+partials in rank order 0..P-1 and rounds once, so every rank holds the same
+bits and the result does not depend on collective algorithm choice.
+Element-wise evaluation alone needs no communication.
+"""
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+from .api import TORCH_DTYPE, Context, Lowered, partial_bytes, shard_range
+
+__all__ = ["shard_range", "column_block", "allgather_partials", "DistReducer"]
+
+
+def column_block(n_cols: int, rank: int, world: int) -> tuple[int, int]:
+    """Columns [c0, c1) of a column-major Mat owned by `rank`."""
+    return shard_range(n_cols, rank, world, 1)
+
+
+def allgather_partials(local: torch.Tensor, group=None) -> torch.Tensor:
+    """Gather every rank's partial (same byte length) into one tensor laid out
+    in rank order.  NCCL: device all_gather_into_tensor on the current stream.
+    Other backends (gloo): staged through host memory."""
+    world = dist.get_world_size(group)
+    flat = local.reshape(-1)
+    if world == 1:
+        return flat.clone()
+    backend = dist.get_backend(group)
+    if backend == "nccl" and flat.is_cuda:
+        out = torch.empty(world * flat.numel(), dtype=flat.dtype, device=flat.device)
+        dist.all_gather_into_tensor(out, flat, group=group)
+        return out
+    host = flat.detach().cpu()
+    parts = [torch.empty_like(host) for _ in range(world)]
+    dist.all_gather(parts, host, group=group)
+    out = torch.cat(parts)
+    return out.to(flat.device, non_blocking=False) if flat.is_cuda else out
+
+
+class DistReducer:
+    """Global reductions over rank-sharded operands: partial -> gather -> combine."""
+
+    def __init__(self, ctx: Context, group=None):
+        self.ctx = ctx
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        dev = ctx.device
+        self._rec = torch.zeros(partial_bytes("ACCU") // 8, dtype=torch.int64, device=dev)
+
+    def reduce(self, lw: Lowered, kind: str, out: torch.Tensor | None = None,
+               kernel_events: list | None = None) -> torch.Tensor:
+        """Full reduction (ACCU/MIN/MAX/MINMAX/NORM2) of this rank's block;
+        returns the GLOBAL result (1 or 2 eT) on every rank."""
+        if kernel_events is not None:
+            e0 = torch.cuda.Event(enable_timing=True)
+            e0.record(self.ctx.stream)
+        self.ctx.reduce_partial(lw.elem, lw.n_rows, lw.n_cols, lw.program, lw.operands,
+                                lw.scalars, kind, self._rec, out)
+        if kernel_events is not None:
+            e1 = torch.cuda.Event(enable_timing=True)
+            e1.record(self.ctx.stream)
+            kernel_events.append((e0, e1))
+        parts = allgather_partials(self._rec, self.group)
+        res = torch.empty(2, dtype=TORCH_DTYPE[lw.elem], device=self.ctx.device)
+        self.ctx.combine(lw.elem, kind, parts, self.world, 1, res)
+        return res
+
+    def sum_dim1_columns(self, lw: Lowered, total_rows: int | None = None) -> torch.Tensor:
+        """sum(X, 1) when ranks own column blocks: every rank's row-sum partial
+        (n_rows f64/u64) is gathered and combined in rank order."""
+        m = lw.n_rows
+        words = partial_bytes("SUM_DIM1", m) // 8
+        part = torch.zeros(words, dtype=torch.int64, device=self.ctx.device)
+        self.ctx.reduce_partial(lw.elem, lw.n_rows, lw.n_cols, lw.program, lw.operands,
+                                lw.scalars, "SUM_DIM1", part)
+        parts = allgather_partials(part, self.group)
+        res = torch.empty(m, dtype=TORCH_DTYPE[lw.elem], device=self.ctx.device)
+        self.ctx.combine(lw.elem, "SUM_DIM1", parts, self.world, m, res)
+        return res
+
+    def sum_dim0_columns(self, lw: Lowered) -> torch.Tensor:
+        """sum(X, 0) when ranks own column blocks: purely local (no exchange);
+        returns this rank's slice of the Row."""
+        res = torch.empty(lw.n_cols, dtype=TORCH_DTYPE[lw.elem], device=self.ctx.device)
+        self.ctx.reduce(lw.elem, lw.n_rows, lw.n_cols, lw.program, lw.operands, lw.scalars,
+                        "SUM_DIM0", res)
+        return res

@@ -1,0 +1,44 @@
+"""GPU-test plumbing: a shared ctx, operand upload with controlled alignment."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+TORCH = {"f32": torch.float32, "f64": torch.float64, "u32": torch.uint32, "s64": torch.int64}
+
+
+def have_gpu() -> bool:
+    return torch.cuda.is_available()
+
+
+requires_gpu = pytest.mark.skipif(not torch.cuda.is_available(), reason="no CUDA device")
+
+
+def to_dev(a: np.ndarray, etype: str, offset: int = 0) -> torch.Tensor:
+    """Upload to cuda:0 starting `offset` elements into a fresh allocation
+    (offset controls the 16-byte misalignment of the data pointer)."""
+    a = np.ascontiguousarray(a, dtype=_np_view(etype))
+    if etype == "u32":
+        t = torch.from_numpy(a.view(np.int32).copy()).view(torch.uint32)
+    else:
+        t = torch.from_numpy(a.copy())
+    base = torch.empty(a.size + offset + 8, dtype=TORCH[etype], device="cuda")
+    dst = base[offset:offset + a.size]
+    dst.copy_(t.to("cuda"))
+    return dst
+
+
+def _np_view(etype):
+    return {"f32": np.float32, "f64": np.float64, "u32": np.uint32, "s64": np.int64}[etype]
+
+
+def empty_dev(n: int, etype: str, offset: int = 0) -> torch.Tensor:
+    base = torch.empty(n + offset + 8, dtype=TORCH[etype], device="cuda")
+    return base[offset:offset + n]
+
+
+def to_host(t: torch.Tensor, etype: str) -> np.ndarray:
+    if etype == "u32":
+        return t.cpu().view(torch.int32).numpy().view(np.uint32)
+    return t.cpu().numpy()
