@@ -10,7 +10,7 @@ import os
 import re
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libcoot.so")
+LIB_PATH = os.environ.get("COOT_LIB_PATH") or os.path.join(HERE, "libcoot.so")
 HEADER = os.path.join(os.path.dirname(HERE), "include", "coot.h")
 
 ABI_VERSION = 1

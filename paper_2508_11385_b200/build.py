@@ -15,15 +15,17 @@ import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
-BUILD = os.path.join(HERE, "build")
-LIB = os.path.join(HERE, "libcoot.so")
+# COOT_LIB_NAME / COOT_EXTRA_FLAGS build tuning variants side by side.
+_VARIANT = os.environ.get("COOT_LIB_NAME", "libcoot.so")
+BUILD = os.path.join(HERE, "build", os.path.splitext(_VARIANT)[0])
+LIB = os.path.join(HERE, _VARIANT)
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 
 NVCC = os.environ.get("NVCC", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-fmad=false", "-ftz=false",
          "-prec-div=true", "-prec-sqrt=true", "--expt-relaxed-constexpr", "-I", INCLUDE,
-         "-Xptxas", "-warn-spills"]
+         "-Xptxas", "-warn-spills"] + os.environ.get("COOT_EXTRA_FLAGS", "").split()
 
 
 def _sources():

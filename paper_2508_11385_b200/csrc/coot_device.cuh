@@ -52,7 +52,9 @@ struct FusedArgs {
   uint32_t kind;      // coot_reduce_kind
   uint32_t n_operands;
   uint32_t n_instr;
-  uint16_t key[COOT_MAX_INSTR];  // interpreter: (op << 8) | (depth << 4) | arg
+  uint32_t tile_units;  // TMA driver: 16-byte units per tile (multiple of 256)
+  uint32_t stages;      // TMA driver: smem pipeline depth
+  uint16_t key[COOT_MAX_INSTR];  // interpreter dispatch index: op * 9 + depth
   uint8_t arg[COOT_MAX_INSTR];
 };
 
@@ -113,6 +115,41 @@ __host__ __device__ constexpr bool op_legal(int op) {
                            op == COOT_OP_DIV);
 }
 
+// ---- f32 exp evaluated in f64 (R6) -------------------------------------------
+// e^x = 2^m * 2^(j/64) * e^r with k = rint(x * 64/ln2) = 64m + j and
+// r = x - k*ln2/64 (Cody-Waite, ln2/64 split hi/lo; |r| <= ln2/128 = 0.0054).
+// e^r - 1 by a degree-6 Taylor polynomial (truncation < 3e-20), 2^(j/64) from a
+// correctly rounded table: total relative error < 2^-52 before the single
+// rounding to f32, so the f32 result is the correctly rounded one except when
+// e^x lies within ~2^-52 (relative) of an f32 rounding boundary.  About 12
+// FP64 operations per element (half the generic f64 exp).
+static __device__ const double kExp2Tab[64] = {
+#include "exp2_table.inc"
+};
+
+__device__ __forceinline__ float exp_f32_via_f64(float xf) {
+  const float xc = fminf(fmaxf(xf, -104.0f), 89.0f);  // e^-104 < 2^-150 -> 0; e^89 -> inf
+  const double x = (double)xc;
+  const double kShift = 0x1.8p52;                            // 1.5 * 2^52: rint trick
+  const double ks = __fma_rn(x, 0x1.71547652b82fep+6, kShift);  // x * 64/ln2 + shift
+  const double k = __dsub_rn(ks, kShift);
+  const int ki = (int)__double2loint(ks);  // k as a 32-bit integer
+  // ln2/64 = C1 + C2 (C1 = RN(ln2/64)); the FMA forms k*C1 exactly
+  const double r = __fma_rn(-k, 0x1.62e42fefa39efp-7, x);
+  const double rr = __fma_rn(-k, 0x1.abc9e3b39803fp-62, r);
+  double p = __fma_rn(rr, 1.0 / 720.0, 1.0 / 120.0);
+  p = __fma_rn(p, rr, 1.0 / 24.0);
+  p = __fma_rn(p, rr, 1.0 / 6.0);
+  p = __fma_rn(p, rr, 0.5);
+  p = __fma_rn(p, rr, 1.0);
+  p = __dmul_rn(p, rr);  // e^r - 1
+  const double t = __ldg(&kExp2Tab[ki & 63]);
+  double y = __fma_rn(t, p, t);  // 2^(j/64) * e^r
+  y = __longlong_as_double(__double_as_longlong(y) + ((long long)(ki >> 6) << 52));
+  const float res = __double2float_rn(y);
+  return (xf != xf) ? xf : res;  // NaN passes through
+}
+
 // ---- element semantics ------------------------------------------------------
 template <int OP>
 __device__ __forceinline__ float un(float a) {
@@ -126,7 +163,7 @@ __device__ __forceinline__ float un(float a) {
   // ~2^-52 relative of an f32 rounding boundary (R6).  This keeps
   // composed expressions bit-identical to the correctly-rounded oracle, where
   // expf/logf (<= 2 / 1 ulp) would let later nodes amplify the difference.
-  else if constexpr (OP == COOT_OP_EXP) return __double2float_rn(exp((double)a));
+  else if constexpr (OP == COOT_OP_EXP) return exp_f32_via_f64(a);
   else if constexpr (OP == COOT_OP_LOG) return __double2float_rn(log((double)a));
   else return a;
 }
@@ -223,6 +260,62 @@ __device__ __forceinline__ void store_unit(T* p, const T (&v)[Unit<T>::W]) {
   uint4 r;
   memcpy(&r, &v[0], 16);
   st16(p, r);
+}
+
+// ---- mbarrier + 1-D TMA bulk copies (cp.async.bulk) -------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+// Block until the phase with the given parity has completed.
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t addr = smem_u32(bar);
+  uint32_t done;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(addr), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+// L2 policy for data that is streamed exactly once.
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+// global -> shared 1-D bulk copy completing `bytes` of transaction on `bar`.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
+      "[%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ uint4 lds16(const void* p) {
+  uint4 r;
+  asm volatile("ld.shared.v4.b32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "r"(smem_u32(p)));
+  return r;
 }
 
 // ---- warp shuffles for 64-bit values ---------------------------------------
@@ -427,15 +520,16 @@ __device__ __forceinline__ void write_final(const Accum<T, ACC>& acc, uint32_t k
 // block total in thread 0 (other threads: unspecified).
 template <class T, int ACC>
 __device__ __forceinline__ Accum<T, ACC> block_reduce(Accum<T, ACC> acc) {
-  __shared__ Accum<T, ACC> ws[kWarps];
+  __shared__ Accum<T, ACC> ws[32];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nwarps = (int)(blockDim.x >> 5);
   acc.warp_reduce();
   if (lane == 0) ws[warp] = acc;
   __syncthreads();
   Accum<T, ACC> r;
   r.init();
   if (warp == 0) {
-    if (lane < kWarps) r = ws[lane];
+    if (lane < nwarps) r = ws[lane];
     r.warp_reduce();
   }
   __syncthreads();

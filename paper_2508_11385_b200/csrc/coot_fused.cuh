@@ -1,18 +1,23 @@
 // K1 (templated catalog) and K2 (warp-uniform register interpreter) fused
-// element-wise + terminal-reduction kernels.  Both share ONE driver loop
-// (fused_kernel) so the element -> thread map and the accumulation order are
-// identical: for the same grid, K1 and K2 produce bit-identical results.
+// element-wise + terminal-reduction kernels.
 //
-// Element -> thread map (deterministic, R14): the n elements are split into
-//   head   [0, head)                    scalar elements up to 16-B alignment
-//   body   [head, head + nunits*W)      16-byte units, unit u -> thread u mod N
-//   tail   [tail_begin, n)              scalar elements
-// N = gridDim.x * 256 threads; each thread walks its units in increasing order
-// (U units per iteration, loads issued together for memory-level parallelism;
-// U does not change the order).  The grid depends only on (n, SM count).
+// Both evaluators run inside the SAME driver loop (fused_tma_kernel by
+// default, fused_kernel as the register-pipelined alternative), so the element
+// -> thread map and the accumulation order are identical: for the same
+// expression and grid, K1 and K2 produce bit-identical results.
+//
+// Element semantics live in coot_device.cuh; operands reach an evaluator
+// through a "source": RegSrc (values already in registers) or SmemSrc (a
+// 16-byte unit in the TMA-staged shared-memory tile, read on LOAD).
 #pragma once
 #include "coot_catalog.h"
 #include "coot_device.cuh"
+
+// Minimum resident CTAs per SM requested from ptxas for catalog kernels of the
+// LDG driver (bounds registers at 65536 / (256 * MINB)).
+#ifndef COOT_CAT_MINB
+#define COOT_CAT_MINB 2
+#endif
 
 namespace coot {
 
@@ -21,6 +26,48 @@ __host__ __device__ constexpr int ins_arg(int c) { return c & 15; }
 __host__ __device__ constexpr bool is_unary_op(int op) {
   return op >= COOT_OP_NEG && op <= COOT_OP_LOG;
 }
+
+// ---- operand sources -----------------------------------------------------------
+template <class T, int K, int W>
+struct RegSrc {
+  const T (&in)[K][W];
+  template <int k>
+  __device__ __forceinline__ void get_c(T (&v)[W]) const {
+#pragma unroll
+    for (int w = 0; w < W; ++w) v[w] = in[k][w];
+  }
+  __device__ __forceinline__ void get(int k, T (&v)[W]) const {
+    switch (k) {
+#define COOT_RS(c)                             \
+  case c:                                      \
+    if constexpr ((c) < K) get_c<(c) < K ? (c) : 0>(v); \
+    break;
+      COOT_RS(0) COOT_RS(1) COOT_RS(2) COOT_RS(3) COOT_RS(4) COOT_RS(5) COOT_RS(6) COOT_RS(7)
+#undef COOT_RS
+      default:
+        break;
+    }
+  }
+};
+
+// UD 16-byte units of operand k: stage + k * stride + (i + j * 256) * 16.
+template <class T, int UD>
+struct SmemSrc {
+  static constexpr int WU = Unit<T>::W;
+  const unsigned char* p;  // = stage base + i * 16
+  uint32_t stride;         // bytes between operands in the stage
+  template <int k>
+  __device__ __forceinline__ void get_c(T (&v)[UD * WU]) const {
+    get(k, v);
+  }
+  __device__ __forceinline__ void get(int k, T (&v)[UD * WU]) const {
+#pragma unroll
+    for (int j = 0; j < UD; ++j) {
+      const uint4 r = lds16(p + (size_t)k * stride + (size_t)j * 256 * 16);
+      memcpy(&v[j * WU], &r, 16);
+    }
+  }
+};
 
 // ---- K1: compile-time program ------------------------------------------------
 template <int... Code>
@@ -43,16 +90,15 @@ struct StaticProg {
 
 template <class T, int W, int SP, int C, int... Rest>
 struct StaticStep {
-  template <int K>
-  __device__ __forceinline__ static void run(T (&st)[COOT_MAX_STACK][W], const T (&in)[K][W],
+  template <class Src>
+  __device__ __forceinline__ static void run(T (&st)[COOT_MAX_STACK][W], const Src& src,
                                              const FusedArgs& a) {
     constexpr int op = ins_op(C), arg = ins_arg(C);
     constexpr int nsp = (op == COOT_OP_LOAD || op == COOT_OP_SCALAR) ? SP + 1
                         : is_unary_op(op)                            ? SP
                                                                      : SP - 1;
     if constexpr (op == COOT_OP_LOAD) {
-#pragma unroll
-      for (int w = 0; w < W; ++w) st[SP][w] = in[arg][w];
+      src.template get_c<arg>(st[SP]);
     } else if constexpr (op == COOT_OP_SCALAR) {
       const T s = scalar_as<T>(a.scalars[arg]);
 #pragma unroll
@@ -64,7 +110,7 @@ struct StaticStep {
 #pragma unroll
       for (int w = 0; w < W; ++w) st[SP - 2][w] = bin<op>(st[SP - 2][w], st[SP - 1][w]);
     }
-    if constexpr (sizeof...(Rest) > 0) StaticStep<T, W, nsp, Rest...>::template run<K>(st, in, a);
+    if constexpr (sizeof...(Rest) > 0) StaticStep<T, W, nsp, Rest...>::run(st, src, a);
   }
 };
 
@@ -74,87 +120,88 @@ template <int... Code>
 struct CatalogEval<StaticProg<Code...>> {
   static constexpr int K = StaticProg<Code...>::n_ops();
   static constexpr bool kInterp = false;
-  template <class T, int W>
-  __device__ __forceinline__ static void eval(const T (&in)[K][W], const FusedArgs& a,
-                                              T (&out)[W]) {
+  template <class T, int W, class Src>
+  __device__ __forceinline__ static void eval_src(const Src& src, const FusedArgs& a, T (&out)[W]) {
     T st[COOT_MAX_STACK][W];
-    StaticStep<T, W, 0, Code...>::template run<K>(st, in, a);
+    StaticStep<T, W, 0, Code...>::run(st, src, a);
 #pragma unroll
     for (int w = 0; w < W; ++w) out[w] = st[0][w];
+  }
+  template <class T, int W>
+  __device__ __forceinline__ static void eval(const T (&in)[K][W], const FusedArgs& a, T (&out)[W]) {
+    eval_src<T, W>(RegSrc<T, K, W>{in}, a, out);
   }
 };
 
 // ---- K2: warp-uniform register interpreter --------------------------------
-// The host precomputes key = (op << 8) | (depth << 4) | arg for every
-// instruction (depth = stack size before it).  The key lives in the kernel's
-// parameter bank and is uniform across the grid, so each `switch` is a
-// uniform branch; every case touches stack registers with compile-time
-// indices (no local memory).  One dispatch handles a whole 16-byte unit.
-#define COOT_KEY(op, d, a) (((op) << 8) | ((d) << 4) | (a))
+// The host precomputes a dense key = op * 9 + depth for every instruction
+// (depth = stack size before it, 0..8).  Keys live in the kernel's parameter
+// bank and are uniform across the grid, so each `switch` (a jump table over
+// 126 dense cases) is a uniform branch; every case touches stack registers
+// with compile-time indices.  LOAD takes its operand index at run time from
+// the source (a shared-memory address under the TMA driver).  One dispatch
+// evaluates a whole 16-byte unit.
+#define COOT_KEY(op, d) ((op) * 9 + (d))
 
 template <int KMAX, int SMAX>
 struct InterpEval {
   static constexpr int K = KMAX;
   static constexpr bool kInterp = true;
 
-  template <class T, int W>
-  __device__ __forceinline__ static void eval(const T (&in)[K][W], const FusedArgs& a,
-                                              T (&out)[W]) {
+  template <class T, int W, class Src>
+  __device__ __forceinline__ static void eval_src(const Src& src, const FusedArgs& a, T (&out)[W]) {
     T st[SMAX][W];  // every slot is written (LOAD/SCALAR) before it is read
 
-#define COOT_LOAD_CASE(d, k)                                               \
-  case COOT_KEY(COOT_OP_LOAD, d, k):                                       \
-    if constexpr ((d) < SMAX && (k) < K) {                                 \
-      _Pragma("unroll") for (int w = 0; w < W; ++w) st[d][w] = in[k][w];   \
-    }                                                                      \
+#define COOT_LOAD_CASE(d)                                                  \
+  case COOT_KEY(COOT_OP_LOAD, d):                                          \
+    if constexpr ((d) < SMAX) src.get((int)a.arg[i], st[(d) < SMAX ? (d) : 0]); \
     break;
 #define COOT_SCALAR_CASE(d)                                                \
-  case COOT_KEY(COOT_OP_SCALAR, d, 0):                                     \
+  case COOT_KEY(COOT_OP_SCALAR, d):                                        \
     if constexpr ((d) < SMAX) {                                            \
       const T s = scalar_as<T>(a.scalars[a.arg[i]]);                       \
       _Pragma("unroll") for (int w = 0; w < W; ++w) st[d][w] = s;          \
     }                                                                      \
     break;
 #define COOT_UN_CASE(OP, d)                                                \
-  case COOT_KEY(COOT_OP_##OP, d, 0):                                       \
+  case COOT_KEY(COOT_OP_##OP, d):                                          \
     if constexpr ((d) >= 1 && (d) <= SMAX && op_legal<T>(COOT_OP_##OP)) {  \
       _Pragma("unroll") for (int w = 0; w < W; ++w)                        \
           st[(d) - 1][w] = un<COOT_OP_##OP>(st[(d) - 1][w]);                \
     }                                                                      \
     break;
 #define COOT_BIN_CASE(OP, d)                                               \
-  case COOT_KEY(COOT_OP_##OP, d, 0):                                       \
+  case COOT_KEY(COOT_OP_##OP, d):                                          \
     if constexpr ((d) >= 2 && (d) <= SMAX && op_legal<T>(COOT_OP_##OP)) {  \
       _Pragma("unroll") for (int w = 0; w < W; ++w)                        \
           st[(d) - 2][w] = bin<COOT_OP_##OP>(st[(d) - 2][w], st[(d) - 1][w]); \
     }                                                                      \
     break;
-#define COOT_CASES_AT(d)                                                             \
-  COOT_LOAD_CASE(d, 0) COOT_LOAD_CASE(d, 1) COOT_LOAD_CASE(d, 2) COOT_LOAD_CASE(d, 3) \
-  COOT_LOAD_CASE(d, 4) COOT_LOAD_CASE(d, 5) COOT_LOAD_CASE(d, 6) COOT_LOAD_CASE(d, 7) \
-  COOT_SCALAR_CASE(d)                                                                \
-  COOT_UN_CASE(NEG, d) COOT_UN_CASE(ABS, d) COOT_UN_CASE(SQUARE, d)                  \
-  COOT_UN_CASE(SQRT, d) COOT_UN_CASE(EXP, d) COOT_UN_CASE(LOG, d)                    \
-  COOT_BIN_CASE(ADD, d) COOT_BIN_CASE(SUB, d) COOT_BIN_CASE(MUL, d)                  \
-  COOT_BIN_CASE(DIV, d) COOT_BIN_CASE(MIN, d) COOT_BIN_CASE(MAX, d)
+#define COOT_D(M, ...) M(__VA_ARGS__ 0) M(__VA_ARGS__ 1) M(__VA_ARGS__ 2) M(__VA_ARGS__ 3) \
+  M(__VA_ARGS__ 4) M(__VA_ARGS__ 5) M(__VA_ARGS__ 6) M(__VA_ARGS__ 7) M(__VA_ARGS__ 8)
 
 #pragma unroll 1
     for (uint32_t i = 0; i < a.n_instr; ++i) {
       switch (a.key[i]) {
-        COOT_CASES_AT(0)
-        COOT_CASES_AT(1)
-        COOT_CASES_AT(2)
-        COOT_CASES_AT(3)
-        COOT_CASES_AT(4)
-        COOT_CASES_AT(5)
-        COOT_CASES_AT(6)
-        COOT_CASES_AT(7)
-        COOT_CASES_AT(8)
+        COOT_D(COOT_LOAD_CASE)
+        COOT_D(COOT_SCALAR_CASE)
+        COOT_D(COOT_UN_CASE, NEG,)
+        COOT_D(COOT_UN_CASE, ABS,)
+        COOT_D(COOT_UN_CASE, SQUARE,)
+        COOT_D(COOT_UN_CASE, SQRT,)
+        COOT_D(COOT_UN_CASE, EXP,)
+        COOT_D(COOT_UN_CASE, LOG,)
+        COOT_D(COOT_BIN_CASE, ADD,)
+        COOT_D(COOT_BIN_CASE, SUB,)
+        COOT_D(COOT_BIN_CASE, MUL,)
+        COOT_D(COOT_BIN_CASE, DIV,)
+        COOT_D(COOT_BIN_CASE, MIN,)
+        COOT_D(COOT_BIN_CASE, MAX,)
         default:
           break;
       }
     }
-#undef COOT_CASES_AT
+#undef COOT_D
 #undef COOT_BIN_CASE
 #undef COOT_UN_CASE
 #undef COOT_SCALAR_CASE
@@ -162,9 +209,13 @@ struct InterpEval {
 #pragma unroll
     for (int w = 0; w < W; ++w) out[w] = st[0][w];
   }
+  template <class T, int W>
+  __device__ __forceinline__ static void eval(const T (&in)[K][W], const FusedArgs& a, T (&out)[W]) {
+    eval_src<T, W>(RegSrc<T, K, W>{in}, a, out);
+  }
 };
 
-// ---- operand loading ------------------------------------------------------
+// ---- operand loading (register drivers) -------------------------------------
 template <class T, class EV>
 __device__ __forceinline__ void load_units(const FusedArgs& a, u64 e,
                                            T (&in)[EV::K][Unit<T>::W]) {
@@ -172,6 +223,17 @@ __device__ __forceinline__ void load_units(const FusedArgs& a, u64 e,
   for (int k = 0; k < EV::K; ++k) {
     if (!EV::kInterp || k < (int)a.n_operands)
       load_unit<T>(reinterpret_cast<const T*>(a.in[k]) + e, in[k]);
+  }
+}
+template <class T, class EV>
+__device__ __forceinline__ void load_units_p(const FusedArgs& a, u64 boff, uint32_t u,
+                                             T (&in)[EV::K][Unit<T>::W]) {
+#pragma unroll
+  for (int k = 0; k < EV::K; ++k) {
+    if (!EV::kInterp || k < (int)a.n_operands) {
+      uint4 r = ld16(reinterpret_cast<const uint4*>(reinterpret_cast<const char*>(a.in[k]) + boff) + u);
+      memcpy(&in[k][0], &r, 16);
+    }
   }
 }
 template <class T, class EV>
@@ -185,9 +247,15 @@ __device__ __forceinline__ void load_elem(const FusedArgs& a, u64 e, T (&in)[EV:
   }
 }
 
-// ---- the shared driver --------------------------------------------------
+// ---- LDG driver (register-pipelined; COOT_DRIVER=0) ---------------------------
+// Element -> thread map: head [0, head) and tail [tail_begin, n) scalars by
+// global thread index; body 16-byte unit u -> thread u mod N (N = grid*256),
+// each thread walking its units in increasing order.  The loads of the NEXT U
+// units are issued before the current ones are evaluated.  The body is walked
+// in segments of SEG units (SEG = 0 mod N, < 2^31) so the loop index is 32-bit.
 template <class T, int ACC, class EV, int U>
-__global__ void __launch_bounds__(kThreads) fused_kernel(const __grid_constant__ FusedArgs a) {
+__global__ void __launch_bounds__(kThreads, EV::kInterp ? 1 : COOT_CAT_MINB)
+    fused_kernel(const __grid_constant__ FusedArgs a) {
   constexpr int W = Unit<T>::W;
   constexpr int K = EV::K;
   Accum<T, ACC> acc;
@@ -196,7 +264,6 @@ __global__ void __launch_bounds__(kThreads) fused_kernel(const __grid_constant__
   const u64 nthr = (u64)gridDim.x * kThreads;
   T* out = reinterpret_cast<T*>(a.out);
 
-  // head (scalar)
   for (u64 e = tid; e < a.head; e += nthr) {
     T in[K][1], v[1];
     load_elem<T, EV>(a, e, in);
@@ -204,36 +271,190 @@ __global__ void __launch_bounds__(kThreads) fused_kernel(const __grid_constant__
     if (out) out[e] = v[0];
     acc.template add<1>(v);
   }
-  // body: 16-byte units
-  u64 u = tid;
-  if constexpr (U > 1) {
-    for (; u + (U - 1) * nthr < a.nunits; u += U * nthr) {
-      T in[U][K][W];
+  {
+    const uint32_t nthr32 = (uint32_t)nthr, tid32 = (uint32_t)tid;
+    const u64 SEG = (u64)(0x7fffffffu / nthr32) * nthr32;
+    for (u64 s0 = 0; s0 < a.nunits; s0 += SEG) {
+      const uint32_t nloc = (uint32_t)((a.nunits - s0) < SEG ? (a.nunits - s0) : SEG);
+      const u64 boff = a.head * sizeof(T) + s0 * 16;
+      uint4* po = out ? reinterpret_cast<uint4*>(reinterpret_cast<char*>(out) + boff) : nullptr;
+      uint32_t u = tid32;
+      T cur[U][K][W];
 #pragma unroll
-      for (int j = 0; j < U; ++j) load_units<T, EV>(a, a.head + (u + j * nthr) * W, in[j]);
+      for (int j = 0; j < U; ++j)
+        if (u + j * nthr32 < nloc) load_units_p<T, EV>(a, boff, u + j * nthr32, cur[j]);
+      while (u < nloc) {
+        const uint32_t un = u + U * nthr32;
+        T nxt[U][K][W];
 #pragma unroll
-      for (int j = 0; j < U; ++j) {
-        T v[W];
-        EV::template eval<T, W>(in[j], a, v);
-        if (out) store_unit<T>(out + a.head + (u + j * nthr) * W, v);
-        acc.template add<W>(v);
+        for (int j = 0; j < U; ++j)
+          if (un + j * nthr32 < nloc) load_units_p<T, EV>(a, boff, un + j * nthr32, nxt[j]);
+#pragma unroll
+        for (int j = 0; j < U; ++j) {
+          if (u + j * nthr32 < nloc) {
+            T v[W];
+            EV::template eval<T, W>(cur[j], a, v);
+            if (po) {
+              uint4 r;
+              memcpy(&r, &v[0], 16);
+              st16(po + u + j * nthr32, r);
+            }
+            acc.template add<W>(v);
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < U; ++j)
+#pragma unroll
+          for (int k = 0; k < K; ++k)
+#pragma unroll
+            for (int w = 0; w < W; ++w) cur[j][k][w] = nxt[j][k][w];
+        u = un;
       }
     }
   }
-  for (; u < a.nunits; u += nthr) {
-    T in[K][W], v[W];
-    load_units<T, EV>(a, a.head + u * W, in);
-    EV::template eval<T, W>(in, a, v);
-    if (out) store_unit<T>(out + a.head + u * W, v);
-    acc.template add<W>(v);
-  }
-  // tail (scalar)
   for (u64 e = a.tail_begin + tid; e < a.n; e += nthr) {
     T in[K][1], v[1];
     load_elem<T, EV>(a, e, in);
     EV::template eval<T, 1>(in, a, v);
     if (out) out[e] = v[0];
     acc.template add<1>(v);
+  }
+
+  if constexpr (ACC != ACC_NONE) {
+    Accum<T, ACC> bt = block_reduce<T, ACC>(acc);
+    grid_finish<T, ACC>(bt, a.partials, a.ticket, a.final_mode, a.kind, a.result, a.count);
+  }
+}
+
+// ---- the TMA-staged driver (default on B200) ---------------------------------
+// One producer warp streams tiles of every operand into a `stages`-deep shared
+// memory ring with 1-D bulk copies (cp.async.bulk + mbarrier complete_tx,
+// L2 evict-first); 8 consumer warps evaluate the program out of shared memory,
+// store the element-wise result and accumulate.  Memory-level parallelism
+// (stages x operands x tile bytes in flight per CTA) does not depend on
+// registers or occupancy, so compute-heavy programs (f64-evaluated EXP) and
+// the interpreter keep HBM busy.
+//
+// Element -> thread map: tile t (tile_units 16-byte units) -> CTA t mod G;
+// unit i of a tile -> consumer thread i mod 256; each thread walks its units
+// tile by tile in increasing order; head/tail scalars -> global consumer
+// thread index.  Depends only on (n, operands, SM count) and is shared by K1
+// and K2, which therefore agree bit for bit.
+constexpr int kConsumerWarps = 8;
+constexpr int kTmaThreads = (kConsumerWarps + 1) * 32;
+// Units evaluated per dispatch: 2 (more ILP, half the interpreter dispatch
+// cost) except for the 8-operand interpreter, whose stack would not fit.
+#ifndef COOT_UD
+#define COOT_UD 2
+#endif
+constexpr int kTileUnits = 2 * kConsumerWarps * 32;  // 512 units = 8 KB per operand
+template <class EV>
+constexpr int units_per_dispatch() {
+  return (EV::kInterp && EV::K > 4) ? 1 : COOT_UD;
+}
+
+template <class T, int ACC, class EV>
+__global__ void __launch_bounds__(kTmaThreads, 2)  // 2 CTAs/SM: <= 112 registers
+    fused_tma_kernel(const __grid_constant__ FusedArgs a) {
+  constexpr int W = Unit<T>::W;
+  constexpr int K = EV::K;
+  extern __shared__ __align__(128) unsigned char smem[];
+  const uint32_t nk = EV::kInterp ? a.n_operands : (uint32_t)K;
+  const uint32_t S = a.stages, TU = a.tile_units;
+  const uint32_t tile_bytes = TU * 16u;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)S * nk * tile_bytes);
+  uint64_t* empty = full + S;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (uint32_t s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kConsumerWarps);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  Accum<T, ACC> acc;
+  acc.init();
+  const u64 ntiles = (a.nunits + TU - 1) / TU;
+  const u64 boff = a.head * sizeof(T);  // body starts 16-byte aligned here
+
+  if (warp == kConsumerWarps) {
+    // ---------------- producer ----------------
+    if (lane == 0) {
+      const uint64_t pol = policy_evict_first();
+      uint32_t s = 0, ph = 0;
+      u64 i = 0;
+      for (u64 t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
+        if (i >= S) mbar_wait(&empty[s], ph ^ 1u);
+        const u64 u0 = t * TU;
+        const uint32_t nu = (uint32_t)((a.nunits - u0) < TU ? (a.nunits - u0) : TU);
+        mbar_expect_tx(&full[s], nu * 16u * nk);
+        for (uint32_t k = 0; k < nk; ++k)
+          bulk_g2s(smem + ((size_t)s * nk + k) * tile_bytes,
+                   reinterpret_cast<const char*>(a.in[k]) + boff + u0 * 16, nu * 16u, &full[s],
+                   pol);
+        if (++s == S) {
+          s = 0;
+          ph ^= 1u;
+        }
+      }
+    }
+  } else {
+    // ---------------- consumers ----------------
+    const u64 ctid = (u64)blockIdx.x * (kConsumerWarps * 32) + threadIdx.x;
+    const u64 cthr = (u64)gridDim.x * (kConsumerWarps * 32);
+    T* out = reinterpret_cast<T*>(a.out);
+    for (u64 e = ctid; e < a.head; e += cthr) {
+      T in[K][1], v[1];
+      load_elem<T, EV>(a, e, in);
+      EV::template eval<T, 1>(in, a, v);
+      if (out) out[e] = v[0];
+      acc.template add<1>(v);
+    }
+    uint4* po = out ? reinterpret_cast<uint4*>(reinterpret_cast<char*>(out) + boff) : nullptr;
+    uint32_t s = 0, ph = 0;
+    for (u64 t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      const u64 u0 = t * TU;
+      const uint32_t nu = (uint32_t)((a.nunits - u0) < TU ? (a.nunits - u0) : TU);
+      mbar_wait(&full[s], ph);
+      const unsigned char* stg = smem + (size_t)s * nk * tile_bytes;
+      // each dispatch evaluates UD units (i, i + 256, ...) of the tile together;
+      // units are stored / accumulated in increasing order
+      constexpr int UD = units_per_dispatch<EV>();
+      for (uint32_t i = threadIdx.x; i < nu; i += UD * kConsumerWarps * 32) {
+        T v[UD * W];
+        EV::template eval_src<T, UD * W>(SmemSrc<T, UD>{stg + (size_t)i * 16, tile_bytes}, a, v);
+#pragma unroll
+        for (int j = 0; j < UD; ++j) {
+          const uint32_t ij = i + j * kConsumerWarps * 32;
+          if (j == 0 || ij < nu) {
+            T vj[W];
+#pragma unroll
+            for (int w = 0; w < W; ++w) vj[w] = v[j * W + w];
+            if (po) {
+              uint4 r;
+              memcpy(&r, &vj[0], 16);
+              st16(po + u0 + ij, r);
+            }
+            acc.template add<W>(vj);
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+      if (++s == S) {
+        s = 0;
+        ph ^= 1u;
+      }
+    }
+    for (u64 e = a.tail_begin + ctid; e < a.n; e += cthr) {
+      T in[K][1], v[1];
+      load_elem<T, EV>(a, e, in);
+      EV::template eval<T, 1>(in, a, v);
+      if (out) out[e] = v[0];
+      acc.template add<1>(v);
+    }
   }
 
   if constexpr (ACC != ACC_NONE) {

@@ -14,6 +14,8 @@ struct FusedPlan {
   int interp_large;  // interpreter size class: 0 = <=4 operands / depth 4, 1 = <=8 / 8
   int acc;           // AccKind
   unsigned grid;
+  int driver;        // 0 = register-pipelined LDG driver, 1 = TMA-staged driver
+  unsigned smem;     // dynamic shared memory (TMA driver)
 };
 
 enum DimKernel { DIMK_DIM0_BLOCK = 0, DIMK_DIM0_WARP = 1, DIMK_DIM1 = 2 };

@@ -1,6 +1,9 @@
 // Kernel tables and launchers, instantiated once per element type in
 // kernels_<type>.cu (so the four type families compile in parallel).
 #pragma once
+#include <mutex>
+#include <unordered_set>
+
 #include "coot_dim.cuh"
 #include "coot_internal.h"
 
@@ -9,55 +12,79 @@ namespace coot {
 typedef void (*FusedFn)(const FusedArgs);
 typedef void (*DimFn)(const DimArgs);
 
-// U (units per thread per iteration, issued together): more for few operands
-// so every thread keeps >= 32-64 bytes of loads in flight.
-constexpr int unroll_for(int k) { return k <= 1 ? 4 : 2; }
+// LDG driver: U units per thread per iteration (prefetched one iteration
+// ahead) so every thread keeps >= 64 bytes of loads in flight.
+constexpr int unroll_for(int k) { return k <= 1 ? 4 : (k == 2 ? 2 : 1); }
+
+template <class T, int ACC, class EV, int U>
+FusedFn driver_kernel(int driver) {
+  if (driver == 1) return &fused_tma_kernel<T, ACC, EV>;
+  return &fused_kernel<T, ACC, EV, U>;
+}
 
 template <class T, int ACC, int... Code>
-FusedFn catalog_kernel() {
+FusedFn catalog_kernel(int driver) {
   typedef StaticProg<Code...> P;
   if constexpr (P::template legal<T>()) {
-    return &fused_kernel<T, ACC, CatalogEval<P>, unroll_for(P::n_ops())>;
+    return driver_kernel<T, ACC, CatalogEval<P>, unroll_for(P::n_ops())>(driver);
   } else {
     return nullptr;
   }
 }
 
 template <class T, int ACC>
-FusedFn pick_fused_acc(int catalog, int interp_large) {
+FusedFn pick_fused_acc(int catalog, int interp_large, int driver) {
   if constexpr (ACC == ACC_SUMSQ && !is_float<T>()) {
     return nullptr;
   } else {
     switch (catalog) {
 #define COOT_X(id, ...) \
   case id:              \
-    return catalog_kernel<T, ACC, __VA_ARGS__>();
+    return catalog_kernel<T, ACC, __VA_ARGS__>(driver);
       COOT_CATALOG(COOT_X)
 #undef COOT_X
       default:
         break;
     }
-    if (interp_large) return &fused_kernel<T, ACC, InterpEval<8, 8>, 1>;
-    return &fused_kernel<T, ACC, InterpEval<4, 4>, 1>;
+    if (interp_large) return driver_kernel<T, ACC, InterpEval<8, 8>, 1>(driver);
+    return driver_kernel<T, ACC, InterpEval<4, 4>, 1>(driver);
   }
 }
 
 template <class T>
 FusedFn pick_fused(const FusedPlan& p) {
   switch (p.acc) {
-    case ACC_NONE: return pick_fused_acc<T, ACC_NONE>(p.catalog, p.interp_large);
-    case ACC_SUM: return pick_fused_acc<T, ACC_SUM>(p.catalog, p.interp_large);
-    case ACC_SUMSQ: return pick_fused_acc<T, ACC_SUMSQ>(p.catalog, p.interp_large);
-    case ACC_MINMAX: return pick_fused_acc<T, ACC_MINMAX>(p.catalog, p.interp_large);
+    case ACC_NONE: return pick_fused_acc<T, ACC_NONE>(p.catalog, p.interp_large, p.driver);
+    case ACC_SUM: return pick_fused_acc<T, ACC_SUM>(p.catalog, p.interp_large, p.driver);
+    case ACC_SUMSQ: return pick_fused_acc<T, ACC_SUMSQ>(p.catalog, p.interp_large, p.driver);
+    case ACC_MINMAX: return pick_fused_acc<T, ACC_MINMAX>(p.catalog, p.interp_large, p.driver);
   }
   return nullptr;
+}
+
+// Opt every TMA-driver kernel into > 48 KB of dynamic shared memory once.
+inline cudaError_t allow_smem(const void* fn, unsigned bytes) {
+  static std::mutex mu;
+  static std::unordered_set<const void*> done;
+  std::lock_guard<std::mutex> lock(mu);
+  if (done.count(fn)) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  if (e == cudaSuccess) done.insert(fn);
+  (void)bytes;
+  return e;
 }
 
 template <class T>
 cudaError_t launch_fused_t(const FusedPlan& p, const FusedArgs& a, cudaStream_t s) {
   FusedFn k = pick_fused<T>(p);
   if (!k) return cudaErrorInvalidDeviceFunction;
-  k<<<p.grid, kThreads, 0, s>>>(a);
+  if (p.driver == 1) {
+    cudaError_t e = allow_smem(reinterpret_cast<const void*>(k), p.smem);
+    if (e != cudaSuccess) return e;
+    k<<<p.grid, kTmaThreads, p.smem, s>>>(a);
+  } else {
+    k<<<p.grid, kThreads, 0, s>>>(a);
+  }
   return cudaGetLastError();
 }
 

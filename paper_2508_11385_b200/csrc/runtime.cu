@@ -28,7 +28,9 @@ struct coot_ctx {
   uint32_t flags = 0;
   int sm_count = 0;
   int cc_major = 0, cc_minor = 0;
-  int blocks_per_sm = 8;
+  int blocks_per_sm = 8;    // LDG driver / dim kernels: CTAs per SM in the grid
+  int driver = 1;           // fused pass: 1 = TMA-staged (default), 0 = LDG
+  int tma_ctas_per_sm = 2;  // TMA driver: CTAs per SM in the grid
   coot::Rec* recs = nullptr;  // per-block records of the fused pass
   unsigned max_grid = 0;
   unsigned* ticket = nullptr;  // fused-pass arrival counter
@@ -212,6 +214,26 @@ coot_status check_result_alias(const coot_expr* e, const void* result, size_t rb
 }
 
 // ---- lowering ---------------------------------------------------------------
+// Drop operands the program never LOADs and renumber the rest (order kept), so
+// every staged / loaded array is one the expression reads.
+coot_expr compact_expr(const coot_expr* e, Shape* sh) {
+  coot_expr c = *e;
+  int remap[COOT_MAX_OPERANDS];
+  uint32_t n = 0;
+  for (uint32_t k = 0; k < e->n_operands; ++k) {
+    remap[k] = -1;
+    if (sh->used_mask & (1u << k)) {
+      remap[k] = (int)n;
+      c.operands[n++] = e->operands[k];
+    }
+  }
+  c.n_operands = n;
+  for (uint32_t i = 0; i < e->n_instr; ++i)
+    if (e->prog[i].op == COOT_OP_LOAD) c.prog[i].arg = (uint8_t)remap[e->prog[i].arg];
+  sh->used_mask = (n >= 32) ? 0xffffffffu : ((1u << n) - 1u);
+  return c;
+}
+
 struct CatalogEntry {
   int id;
   int n;
@@ -248,7 +270,7 @@ void fill_program(const coot_expr* e, coot::FusedArgs* a) {
   int sp = 0;
   for (uint32_t i = 0; i < e->n_instr; ++i) {
     const int op = e->prog[i].op, arg = e->prog[i].arg;
-    a->key[i] = (uint16_t)COOT_KEY(op, sp, op == COOT_OP_LOAD ? arg : 0);
+    a->key[i] = (uint16_t)COOT_KEY(op, sp);  // dense dispatch index (coot_fused.cuh)
     a->arg[i] = (uint8_t)arg;
     if (op == COOT_OP_LOAD || op == COOT_OP_SCALAR) ++sp;
     else if (is_binary(op)) --sp;
@@ -371,9 +393,28 @@ coot_status run_fused(coot_ctx* ctx, const coot_expr* e, const Shape& sh, int ac
     a.nunits = 0;
     a.tail_begin = n;
   }
-  const u64 work = std::max<u64>(std::max<u64>(a.nunits, a.head), n - a.tail_begin);
-  u64 grid = std::max<u64>(1, ceil_div(work, coot::kThreads));
-  grid = std::min<u64>(grid, (u64)ctx->sm_count * ctx->blocks_per_sm);
+  const u64 scalar_work = std::max<u64>(a.head, n - a.tail_begin);
+  coot::FusedPlan p;
+  p.driver = ctx->driver;
+  p.smem = 0;
+  u64 grid;
+  if (p.driver == 1) {
+    // TMA driver geometry: a function of (n, operands, SM count) only.
+    const u64 nk = e->n_operands;  // compacted: every operand is referenced
+    const u64 tu = coot::kTileUnits;
+    const u64 tile_bytes_all = nk * tu * 16;
+    const u64 stages = std::max<u64>(2, std::min<u64>(8, (96u << 10) / tile_bytes_all));
+    a.tile_units = (uint32_t)tu;
+    a.stages = (uint32_t)stages;
+    p.smem = (unsigned)(stages * tile_bytes_all + 2 * stages * 8);
+    const u64 ntiles = ceil_div(a.nunits, tu);
+    grid = std::max<u64>(ntiles, ceil_div(scalar_work, coot::kConsumerWarps * 32));
+    grid = std::max<u64>(1, std::min<u64>(grid, (u64)ctx->sm_count * ctx->tma_ctas_per_sm));
+  } else {
+    const u64 work = std::max<u64>(a.nunits, scalar_work);
+    grid = std::max<u64>(1, ceil_div(work, coot::kThreads));
+    grid = std::min<u64>(grid, (u64)ctx->sm_count * ctx->blocks_per_sm);
+  }
   a.partials = ctx->recs;
   a.ticket = ctx->ticket;
   a.result = result;
@@ -381,15 +422,15 @@ coot_status run_fused(coot_ctx* ctx, const coot_expr* e, const Shape& sh, int ac
   a.final_mode = final_mode;
   a.kind = kind;
 
-  coot::FusedPlan p;
   p.catalog = (ctx->flags & COOT_INIT_FORCE_INTERP) ? -1 : match_catalog(e);
   p.interp_large = (e->n_operands > 4 || sh.max_depth > 4) ? 1 : 0;
   p.acc = acc;
   p.grid = (unsigned)grid;
   if (ctx->log)
-    fprintf(stderr, "[coot] fused elem=%u n=%llu path=%d%s acc=%d grid=%u head=%llu units=%llu\n",
+    fprintf(stderr, "[coot] fused elem=%u n=%llu path=%d%s acc=%d driver=%d grid=%u smem=%u stages=%u tile=%u head=%llu units=%llu\n",
             e->elem, (unsigned long long)n, p.catalog, p.catalog < 0 ? (p.interp_large ? "(interp8)" : "(interp4)") : "",
-            acc, p.grid, (unsigned long long)a.head, (unsigned long long)a.nunits);
+            acc, p.driver, p.grid, p.smem, a.stages, a.tile_units, (unsigned long long)a.head,
+            (unsigned long long)a.nunits);
   cudaError_t ce = dispatch_fused(e->elem, p, a, ctx->stream);
   if (ce != cudaSuccess) return cuda_fail(ce, "fused kernel launch");
   ctx->stats.launches++;
@@ -526,7 +567,8 @@ coot_status reduce_common(coot_ctx* ctx, const coot_expr* e, uint32_t kind, void
   if (st != COOT_OK) return st;
   st = bind_device(ctx);
   if (st != COOT_OK) return st;
-  if (dim) return run_dim(ctx, e, sh, kind, result, final_mode);
+  const coot_expr ce = compact_expr(e, &sh);
+  if (dim) return run_dim(ctx, &ce, sh, kind, result, final_mode);
   const int acc = acc_for_kind(kind);
   if (n == 0) {
     if (final_mode == coot::FINAL_PARTIAL) {
@@ -545,7 +587,7 @@ coot_status reduce_common(coot_ctx* ctx, const coot_expr* e, uint32_t kind, void
     if (ce != cudaSuccess) return cuda_fail(ce, "cudaMemsetAsync");
     return ok();
   }
-  return run_fused(ctx, e, sh, acc, kind, result, final_mode, out);
+  return run_fused(ctx, &ce, sh, acc, kind, result, final_mode, out);
 }
 
 }  // namespace
@@ -599,6 +641,8 @@ coot_status coot_init(coot_ctx** out, int device, void* cuda_stream, uint32_t fl
                 device, maj, min);
   }
   ctx->blocks_per_sm = std::max(1, std::min(32, env_int("COOT_BLOCKS_PER_SM", 8)));
+  ctx->driver = env_int("COOT_DRIVER", 1) ? 1 : 0;
+  ctx->tma_ctas_per_sm = std::max(1, std::min(4, env_int("COOT_TMA_CTAS", 2)));
   ctx->max_grid = (unsigned)ctx->sm_count * 32u;
   e = cudaMalloc(&ctx->recs, sizeof(coot::Rec) * ctx->max_grid);
   if (e == cudaSuccess) e = cudaMalloc(&ctx->ticket, 64 * sizeof(unsigned));
@@ -661,7 +705,8 @@ coot_status coot_eval(coot_ctx* ctx, const coot_expr* e, void* out) {
     return fail(COOT_ERR_CONTRACT, "contract: out is not aligned to its element size");
   st = bind_device(ctx);
   if (st != COOT_OK) return st;
-  return run_fused(ctx, e, sh, coot::ACC_NONE, COOT_RED_ACCU, nullptr, coot::FINAL_ROUND, out);
+  const coot_expr ce = compact_expr(e, &sh);
+  return run_fused(ctx, &ce, sh, coot::ACC_NONE, COOT_RED_ACCU, nullptr, coot::FINAL_ROUND, out);
 }
 
 coot_status coot_reduce(coot_ctx* ctx, const coot_expr* e, uint32_t kind, void* result,
