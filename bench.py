@@ -188,8 +188,8 @@ def cpu_baseline_oracle():
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
-    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=2000)
+    ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--impl", default="coot", choices=["coot", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -376,7 +376,7 @@ def main():
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": _traffic(),
                      "peak_kind": peak_kind,
-                     "kernel": "fused_kernel<float, ACC_SUM, catalog 2> (c2 program)",
+                     "kernel": "fused_tma_kernel<float, ACC_SUM, catalog 2> (c2 program)",
                      "alg_bytes_per_launch": alg_bytes, "kernel_ms": kern_ms},
         "cpu_baseline": cpu,
         "e2e": e2e,

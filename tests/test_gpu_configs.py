@@ -1,0 +1,184 @@
+"""Parity at BASELINE.json's FULL sizes, in the launch configuration bench.py
+times (default ctx on cuda:0).  Where the oracle cannot finish in seconds the
+check is on sampled outputs the oracle computes one by one (columns, rows,
+chunks, one shard) plus properties that hold at any size (shard consistency,
+closed forms)."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from gpu_util import TORCH, requires_gpu, to_host
+from progs import C1_AXPY, C2, C4, assert_elementwise, assert_reduction
+
+pytestmark = [pytest.mark.gpu, requires_gpu]
+
+
+@pytest.fixture(scope="module")
+def coot():
+    import paper_2508_11385_b200 as c
+    return c
+
+
+@pytest.fixture(scope="module")
+def ctx(coot):
+    return coot.Context(0)
+
+
+def dev_fill(ctx, etype, n, stream, start=0, n_rows=1, kind="randu"):
+    t = torch.empty(n, dtype=TORCH[etype], device="cuda")
+    ctx.fill(t, kind, stream=stream, start=start, n_rows=n_rows)
+    return t
+
+
+def test_c1_axpy_in_place_then_accu(ctx):
+    """configs[0]: y = 2.5*x + y then accu(y), f32 Col n = 1e6 (in place)."""
+    n = 1_000_000
+    x, y = dev_fill(ctx, "f32", n, 0), dev_fill(ctx, "f32", n, 1)
+    r = torch.zeros(2, device="cuda")
+    ctx.reduce("f32", n, 1, C1_AXPY, [x, y], [2.5], "ACCU", r, y)  # out aliases y
+    torch.cuda.synchronize()
+    acc, z = oracle.run_chunked("f32", C1_AXPY, ["randu", "randu"], start=0, count=n,
+                                scalars=[2.5], kind="ACCU", want_out=True)
+    assert_elementwise(to_host(y, "f32"), z, "f32", max_ulp=0)
+    assert_reduction(r[0].item(), acc, "f32", "ACCU")
+
+
+@pytest.mark.parametrize("store", [True, False])
+def test_c2_full(ctx, store):
+    """configs[1]: Z = exp(A % B) + 3*C then accu(Z), 10000 x 10000 f32."""
+    m = n = 10_000
+    ops = [dev_fill(ctx, "f32", m * n, s, n_rows=m) for s in range(3)]
+    Z = torch.empty(m * n, device="cuda") if store else None
+    r = torch.zeros(2, device="cuda")
+    ctx.reduce("f32", m, n, C2, ops, [3.0], "ACCU", r, Z)
+    torch.cuda.synchronize()
+    acc, z = oracle.run_chunked("f32", C2, ["randu"] * 3, start=0, count=m * n, n_rows=m,
+                                scalars=[3.0], kind="ACCU", want_out=store)
+    assert_reduction(r[0].item(), acc, "f32", "ACCU")
+    if store:
+        assert_elementwise(to_host(Z, "f32"), z, "f32", max_ulp=2)
+    # statistical wiring check: E[Z] = Ei(1) - gamma + 1.5 = 2.8179 (sd 9.25e-5 at 1e8)
+    assert abs(r[0].item() / (m * n) - 2.8179021514544039) < 1e-3
+
+
+def test_c3_sum_dims_full(ctx):
+    """configs[2]: sum(X,0), sum(X,1) on a 32768 x 32768 f64 column-major Mat."""
+    m = n = 32768
+    X = dev_fill(ctx, "f64", m * n, 0, n_rows=m)
+    d0 = torch.empty(n, dtype=torch.float64, device="cuda")
+    d1 = torch.empty(m, dtype=torch.float64, device="cuda")
+    tot = torch.empty(2, dtype=torch.float64, device="cuda")
+    ctx.reduce("f64", m, n, [("LOAD", 0)], [X], [], "SUM_DIM0", d0)
+    ctx.reduce("f64", m, n, [("LOAD", 0)], [X], [], "SUM_DIM1", d1)
+    ctx.reduce("f64", m, n, [("LOAD", 0)], [X], [], "ACCU", tot)
+    torch.cuda.synchronize()
+    d0h, d1h = d0.cpu().numpy(), d1.cpu().numpy()
+    rng = np.random.default_rng(0)
+    # sampled columns: the oracle sums each column from its own regenerated data
+    for j in list(rng.integers(0, n, 12)) + [0, n - 1]:
+        col = oracle.fill("f64", "randu", m, stream=0, start=int(j) * m)
+        assert_reduction(d0h[j], oracle.reduce("f64", "ACCU", col), "f64", "ACCU")
+    # sampled rows: regenerate the matrix chunk by chunk, feed each sampled row in
+    # column order to an oracle accumulator (exactly the oracle's dim-1 order)
+    rows = sorted(set([0, m - 1] + list(rng.integers(0, m, 6))))
+    accs = {i: oracle.Accumulator("f64", "ACCU") for i in rows}
+    step = 2048
+    for c0 in range(0, n, step):
+        chunk = oracle.fill("f64", "randu", m * step, stream=0, start=c0 * m).reshape(step, m)
+        for i in rows:
+            accs[i].add(chunk[:, i])
+    for i in rows:
+        assert_reduction(d1h[i], accs[i].final(), "f64", "ACCU")
+    # invariant: accu(sum(X,0)) == accu(sum(X,1)) == accu(X) within 1e-12
+    t = float(tot[0].item())
+    assert abs(d0h.sum() - t) <= 1e-12 * t and abs(d1h.sum() - t) <= 1e-12 * t
+
+
+_C4_ORACLE = {}
+
+
+@pytest.mark.parametrize("etype", ["u32", "s64"])
+@pytest.mark.parametrize("store", [False, True])
+def test_c4_full_bit_exact(ctx, etype, store):
+    """configs[3]: X % Y + 7*Z with min/max reduction, 2^28 elements, bit-exact."""
+    n = 1 << 28
+    ops = [dev_fill(ctx, etype, n, s) for s in range(3)]
+    out = torch.empty(n, dtype=TORCH[etype], device="cuda") if store else None
+    r = torch.zeros(2, dtype=TORCH[etype], device="cuda")
+    ctx.reduce(etype, n, 1, C4, ops, [7], "MINMAX", r, out)
+    torch.cuda.synchronize()
+    if etype not in _C4_ORACLE:
+        _C4_ORACLE[etype], _ = oracle.run_chunked(etype, C4, ["randu"] * 3, start=0, count=n,
+                                                  scalars=[7], kind="MINMAX")
+    assert np.array_equal(to_host(r, etype), _C4_ORACLE[etype])
+    if store:  # element-wise on the first, a middle and the last 2^22 elements
+        for s0 in (0, n // 2 + 12345, n - (1 << 22)):
+            _, z = oracle.run_chunked(etype, C4, ["randu"] * 3, start=s0, count=1 << 22,
+                                      scalars=[7], want_out=True)
+            assert np.array_equal(to_host(out[s0:s0 + (1 << 22)], etype), z)
+
+
+def _shard_consistency(coot, ctx, etype, prog, ops, sc, kind, n, nparts=16):
+    parts = torch.zeros(nparts * 4, dtype=torch.int64, device="cuda")
+    for r in range(nparts):
+        b, e = coot.shard_range(n, r, nparts, 16)
+        ctx.reduce_partial(etype, e - b, 1, prog, [o[b:e] for o in ops], sc, kind,
+                           parts[4 * r:4 * r + 4])
+    res = torch.zeros(2, dtype=TORCH[etype], device="cuda")
+    ctx.combine(etype, kind, parts, nparts, 1, res)
+    return res
+
+
+@pytest.mark.parametrize("kind", ["dot", "norm2"])
+def test_c5_full_2p32(coot, ctx, kind):
+    """configs[4]: dot(x, y) and norm2(x) on 2^32-element f32 Cols (one GPU holds
+    the whole vector here; the row-block sharding is exercised by the shard
+    checks).  Closed form on ones; randu: one 2^28 shard vs the oracle, and the
+    full launch vs the rank-order combine of 16 shard partials."""
+    n = 1 << 32
+    prog = [("LOAD", 0), ("LOAD", 1), ("MUL", 0)] if kind == "dot" else [("LOAD", 0)]
+    red = "ACCU" if kind == "dot" else "NORM2"
+    k = 2 if kind == "dot" else 1
+    ones = torch.ones(n, device="cuda")
+    r = torch.zeros(2, device="cuda")
+    ctx.reduce("f32", n, 1, prog, [ones] * k, [], red, r)
+    torch.cuda.synchronize()
+    assert r[0].item() == (float(n) if kind == "dot" else 65536.0)  # dot(1,1)=n, |1|=2^16
+    del ones
+    ops = [dev_fill(ctx, "f32", n, s) for s in range(k)]
+    ctx.reduce("f32", n, 1, prog, ops, [], red, r)
+    full = r[0].item()
+    res = _shard_consistency(coot, ctx, "f32", prog, ops, [], red, n)
+    torch.cuda.synchronize()
+    assert abs(res[0].item() - full) <= 1e-5 * abs(full)
+    # one 2^28 shard against the oracle (its own launch on the shard view)
+    s0, cnt = 3 << 28, 1 << 28
+    ctx.reduce("f32", cnt, 1, prog, [o[s0:s0 + cnt] for o in ops], [], red, r)
+    torch.cuda.synchronize()
+    want, _ = oracle.run_chunked("f32", prog, ["randu"] * k, start=s0, count=cnt, kind=red)
+    assert_reduction(r[0].item(), want, "f32", red)
+    # statistical wiring: E[xy] = 1/4, E[x^2] = 1/3
+    expect = n / 4 if kind == "dot" else (n / 3) ** 0.5
+    assert abs(full / expect - 1) < 1e-3
+
+
+@pytest.mark.parametrize("form", ["c2_reduce", "axpy"])
+def test_headline_2p30(coot, ctx, form):
+    """north-star target size: f32 expression + accu on 2^30 elements."""
+    n = 1 << 30
+    prog, sc, k = (C2, [3.0], 3) if form == "c2_reduce" else (C1_AXPY, [2.5], 2)
+    ops = [dev_fill(ctx, "f32", n, s) for s in range(k)]
+    r = torch.zeros(2, device="cuda")
+    ctx.reduce("f32", n, 1, prog, ops, sc, "ACCU", r)
+    torch.cuda.synchronize()
+    full = r[0].item()
+    res = _shard_consistency(coot, ctx, "f32", prog, ops, sc, "ACCU", n)
+    torch.cuda.synchronize()
+    assert abs(res[0].item() - full) <= 1e-5 * abs(full)
+    s0, cnt = 5 << 26, 1 << 26
+    ctx.reduce("f32", cnt, 1, prog, [o[s0:s0 + cnt] for o in ops], sc, "ACCU", r)
+    torch.cuda.synchronize()
+    want, _ = oracle.run_chunked("f32", prog, ["randu"] * k, start=s0, count=cnt, scalars=sc,
+                                 kind="ACCU")
+    assert_reduction(r[0].item(), want, "f32", "ACCU")
