@@ -28,6 +28,7 @@ struct DimArgs {
   u64 ccols;            // dim1: columns per chunk
   uint32_t nchunks;     // dim1: column chunks (1 = no split)
   uint32_t nrt;         // dim1: row tiles
+  uint32_t cg;          // dim1 TMA: columns per pipeline stage
 };
 
 template <class T>

@@ -352,9 +352,15 @@ template <class EV>
 constexpr int units_per_dispatch() {
   return (EV::kInterp && EV::K > 4) ? 1 : COOT_UD;
 }
+// Resident CTAs per SM the register budget is sized for: 2 (<= 96 registers),
+// except the 8-operand interpreter, which gets the whole register file.
+template <class EV>
+constexpr int tma_min_ctas() {
+  return (EV::kInterp && EV::K > 4) ? 1 : 2;
+}
 
 template <class T, int ACC, class EV>
-__global__ void __launch_bounds__(kTmaThreads, 2)  // 2 CTAs/SM: <= 112 registers
+__global__ void __launch_bounds__(kTmaThreads, tma_min_ctas<EV>())
     fused_tma_kernel(const __grid_constant__ FusedArgs a) {
   constexpr int W = Unit<T>::W;
   constexpr int K = EV::K;

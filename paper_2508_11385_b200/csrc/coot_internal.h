@@ -18,13 +18,17 @@ struct FusedPlan {
   unsigned smem;     // dynamic shared memory (TMA driver)
 };
 
-enum DimKernel { DIMK_DIM0_BLOCK = 0, DIMK_DIM0_WARP = 1, DIMK_DIM1 = 2 };
+enum DimKernel {
+  DIMK_DIM0_BLOCK = 0, DIMK_DIM0_WARP = 1, DIMK_DIM1 = 2,  // LDG kernels
+  DIMK_DIM0_TMA = 3, DIMK_DIM1_TMA = 4                     // TMA-staged kernels
+};
 
 struct DimPlan {
   int kernel;        // DimKernel
   int catalog;       // 0 = plain [L0] matrix, -1 interpreter
   int interp_large;
   unsigned grid;
+  unsigned smem;     // dynamic shared memory (TMA kernels)
 };
 
 template <class T>

@@ -5,6 +5,7 @@
 #include <unordered_set>
 
 #include "coot_dim.cuh"
+#include "coot_dim_tma.cuh"
 #include "coot_internal.h"
 
 namespace coot {
@@ -108,17 +109,34 @@ template <class T, class EV>
 struct Dim1 {
   static constexpr DimFn run = &dim1_kernel<T, EV>;
 };
+template <class T, class EV>
+struct Dim0Tma {
+  static constexpr DimFn run = &dim0_tma_kernel<T, EV>;
+};
+template <class T, class EV>
+struct Dim1Tma {
+  static constexpr DimFn run = &dim1_tma_kernel<T, EV>;
+};
 
 template <class T>
 cudaError_t launch_dim_t(const DimPlan& p, const DimArgs& a, cudaStream_t s) {
   DimFn k = nullptr;
+  bool tma = false;
   switch (p.kernel) {
     case DIMK_DIM0_BLOCK: k = pick_dim_ev<T, Dim0Block>(p); break;
     case DIMK_DIM0_WARP: k = pick_dim_ev<T, Dim0Warp>(p); break;
     case DIMK_DIM1: k = pick_dim_ev<T, Dim1>(p); break;
+    case DIMK_DIM0_TMA: k = pick_dim_ev<T, Dim0Tma>(p); tma = true; break;
+    case DIMK_DIM1_TMA: k = pick_dim_ev<T, Dim1Tma>(p); tma = true; break;
   }
   if (!k) return cudaErrorInvalidDeviceFunction;
-  k<<<p.grid, kThreads, 0, s>>>(a);
+  if (tma) {
+    cudaError_t e = allow_smem(reinterpret_cast<const void*>(k), p.smem);
+    if (e != cudaSuccess) return e;
+    k<<<p.grid, kTmaThreads, p.smem, s>>>(a);
+  } else {
+    k<<<p.grid, kThreads, 0, s>>>(a);
+  }
   return cudaGetLastError();
 }
 

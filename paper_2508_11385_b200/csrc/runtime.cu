@@ -31,6 +31,7 @@ struct coot_ctx {
   int blocks_per_sm = 8;    // LDG driver / dim kernels: CTAs per SM in the grid
   int driver = 1;           // fused pass: 1 = TMA-staged (default), 0 = LDG
   int tma_ctas_per_sm = 2;  // TMA driver: CTAs per SM in the grid
+  int dim_tma = 0;          // sum(X,dim): TMA-staged kernels when the layout allows
   coot::Rec* recs = nullptr;  // per-block records of the fused pass
   unsigned max_grid = 0;
   unsigned* ticket = nullptr;  // fused-pass arrival counter
@@ -472,8 +473,58 @@ coot_status run_dim(coot_ctx* ctx, const coot_expr* e, const Shape& sh, uint32_t
   coot::DimPlan p;
   p.catalog = ((ctx->flags & COOT_INIT_FORCE_INTERP) == 0 && e->n_instr == 1) ? 0 : -1;
   p.interp_large = (e->n_operands > 4 || sh.max_depth > 4) ? 1 : 0;
+  p.smem = 0;
   size_t part_bytes = 0, ntickets = 0;
-  if (kind == COOT_RED_SUM_DIM0) {
+  const bool use_tma = ctx->driver == 1 && ctx->dim_tma;
+  const u64 G = (u64)ctx->sm_count * ctx->tma_ctas_per_sm;  // TMA grid: persistent CTAs
+  const u64 nk = e->n_operands;
+  const u64 R1 = (u64)coot::kConsumerWarps * 32 * W;         // dim1 TMA rows per tile
+  if (kind == COOT_RED_SUM_DIM0 && use_tma && same && col_aligned && m * es >= 4096) {
+    // TMA dim 0: pieces = (column, segment), ~8 pieces per CTA, segments >= 1 tile
+    p.kernel = coot::DIMK_DIM0_TMA;
+    d.vec_ok = 1;
+    const u64 tile_el = (u64)coot::kTileUnits * W;
+    u64 S = std::max<u64>(1, ceil_div(8 * G, n));
+    S = std::min<u64>(S, std::max<u64>(1, m / tile_el));
+    u64 L = ceil_div(ceil_div(m, S), tile_el) * tile_el;
+    S = ceil_div(m, L);
+    d.seg_len = L;
+    d.nseg = (uint32_t)S;
+    const u64 stage_bytes = nk * coot::kTileUnits * 16;
+    const u64 stages = std::max<u64>(2, std::min<u64>(8, (96u << 10) / stage_bytes));
+    d.f.tile_units = coot::kTileUnits;
+    d.f.stages = (uint32_t)stages;
+    p.smem = (unsigned)(stages * stage_bytes + 16 * stages);
+    p.grid = (unsigned)std::min<u64>(n * S, G);
+    if (S > 1) {
+      part_bytes = n * S * sbytes;
+      ntickets = n;
+    }
+  } else if (kind == COOT_RED_SUM_DIM1 && use_tma && same && mis == 0 && col_aligned &&
+             m >= R1 / 2) {
+    // TMA dim 1: pieces = (row tile of R1 rows, column chunk), ~8 pieces per CTA
+    p.kernel = coot::DIMK_DIM1_TMA;
+    d.vec_ok = 1;
+    const u64 cg = 4;
+    const u64 nrt = ceil_div(m, R1);
+    u64 nchunks = std::max<u64>(1, ceil_div(8 * G, nrt));
+    nchunks = std::min<u64>(nchunks, std::max<u64>(1, n / (4 * cg)));
+    const u64 ccols = ceil_div(n, nchunks);
+    nchunks = ceil_div(n, ccols);
+    d.cg = (uint32_t)cg;
+    d.nrt = (uint32_t)nrt;
+    d.ccols = ccols;
+    d.nchunks = (uint32_t)nchunks;
+    const u64 stage_bytes = nk * cg * R1 * es;
+    const u64 stages = std::max<u64>(2, std::min<u64>(8, (96u << 10) / stage_bytes));
+    d.f.stages = (uint32_t)stages;
+    p.smem = (unsigned)(stages * stage_bytes + 16 * stages);
+    p.grid = (unsigned)std::min<u64>(nrt * nchunks, G);
+    if (nchunks > 1) {
+      part_bytes = nchunks * m * sbytes;
+      ntickets = nrt;
+    }
+  } else if (kind == COOT_RED_SUM_DIM0) {
     d.vec_ok = (same && col_aligned) ? 1 : 0;
     if (m >= 2048) {
       p.kernel = coot::DIMK_DIM0_BLOCK;
@@ -500,11 +551,13 @@ coot_status run_dim(coot_ctx* ctx, const coot_expr* e, const Shape& sh, uint32_t
     d.vec_ok = (same && mis == 0 && col_aligned) ? 1 : 0;
     uint32_t tpr = 32;
     while (tpr < (uint32_t)coot::kThreads && (u64)tpr * W < m) tpr *= 2;
-    const u64 G = coot::kThreads / tpr;
+    const u64 Gc = coot::kThreads / tpr;  // column groups per CTA
     const u64 R = (u64)tpr * W;
     const u64 nrt = ceil_div(m, R);
-    u64 nchunks = std::max<u64>(1, ceil_div(target, nrt));
-    nchunks = std::min<u64>(nchunks, std::max<u64>(1, n / (8 * G)));
+    // one CTA per (row tile, chunk): keep the grid within one resident wave
+    // (floor, not ceil) so no small tail wave is left over
+    u64 nchunks = std::max<u64>(1, target / nrt);
+    nchunks = std::min<u64>(nchunks, std::max<u64>(1, n / (8 * Gc)));
     const u64 ccols = ceil_div(n, nchunks);
     nchunks = ceil_div(n, ccols);
     d.tpr = tpr;
@@ -643,6 +696,9 @@ coot_status coot_init(coot_ctx** out, int device, void* cuda_stream, uint32_t fl
   ctx->blocks_per_sm = std::max(1, std::min(32, env_int("COOT_BLOCKS_PER_SM", 8)));
   ctx->driver = env_int("COOT_DRIVER", 1) ? 1 : 0;
   ctx->tma_ctas_per_sm = std::max(1, std::min(4, env_int("COOT_TMA_CTAS", 2)));
+  // dim sums default to the LDG kernels: measured faster on B200 (c3: dim0
+  // 7.25 vs 7.04 TB/s, dim1 7.07 vs 6.74 TB/s)
+  ctx->dim_tma = env_int("COOT_DIM_TMA", 0) ? 1 : 0;
   ctx->max_grid = (unsigned)ctx->sm_count * 32u;
   e = cudaMalloc(&ctx->recs, sizeof(coot::Rec) * ctx->max_grid);
   if (e == cudaSuccess) e = cudaMalloc(&ctx->ticket, 64 * sizeof(unsigned));

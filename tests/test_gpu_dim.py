@@ -150,3 +150,43 @@ def test_sum_dim_partial_combine_column_shards(coot, ctx, dim):
             ctx.reduce("f64", m, c1 - c0, P("L0"), [Xd[c0 * m:c1 * m]], [], "SUM_DIM0", res[c0:c1])
         torch.cuda.synchronize()
         _check_vec(to_host(res, "f64"), want, "f64", X, m, n, 0)
+
+
+@pytest.fixture(scope="module")
+def ctx_tma(coot):
+    """A ctx on the TMA-staged dim kernels (COOT_DIM_TMA=1, read at coot_init)."""
+    import os
+    old = os.environ.get("COOT_DIM_TMA")
+    os.environ["COOT_DIM_TMA"] = "1"
+    try:
+        c = coot.Context(0)
+    finally:
+        if old is None:
+            os.environ.pop("COOT_DIM_TMA", None)
+        else:
+            os.environ["COOT_DIM_TMA"] = old
+    return c
+
+
+@pytest.mark.parametrize("etype", ALL)
+@pytest.mark.parametrize("shape", [(4096, 1000), (20000, 3), (513, 513), (2048, 9), (1024, 77),
+                                   (8192, 33)])
+@pytest.mark.parametrize("dim", [0, 1])
+def test_sum_dim_tma_kernels(ctx_tma, etype, shape, dim):
+    m, n = shape
+    X = oracle.fill(etype, "randu", m * n, stream=6)
+    want = oracle.sum_dim(etype, dim, X, m, n)
+    got = run_dim(ctx_tma, etype, P("L0"), [X], [], m, n, dim)
+    _check_vec(got, want, etype, X, m, n, dim)
+
+
+@pytest.mark.parametrize("etype", ["f32", "u32"])
+@pytest.mark.parametrize("dim", [0, 1])
+def test_sum_dim_tma_fused_expression(ctx_tma, etype, dim):
+    m, n = 4096, 203
+    prog = P("L0 L1 MUL S0 L2 MUL ADD")
+    ops = [oracle.fill(etype, "randu", m * n, stream=s) for s in range(3)]
+    Z = oracle.eval_program(etype, prog, ops, [3])
+    want = oracle.sum_dim(etype, dim, Z, m, n)
+    got = run_dim(ctx_tma, etype, prog, ops, [3], m, n, dim)
+    _check_vec(got, want, etype, Z, m, n, dim)

@@ -322,3 +322,43 @@ def test_simulated_shards_partial_combine(coot, ctx, etype, kind):
         got = to_host(res, etype)
         got = got[:2] if kind == "MINMAX" else got[0]
         assert_reduction(got, want, etype, kind, abs_scale(want_z))
+
+
+@pytest.fixture(scope="module")
+def ctx_ldg(coot):
+    """A ctx on the register-pipelined LDG driver (COOT_DRIVER=0 at coot_init)."""
+    import os
+    old = os.environ.get("COOT_DRIVER")
+    os.environ["COOT_DRIVER"] = "0"
+    try:
+        c = coot.Context(0)
+    finally:
+        if old is None:
+            os.environ.pop("COOT_DRIVER", None)
+        else:
+            os.environ["COOT_DRIVER"] = old
+    return c
+
+
+@pytest.mark.parametrize("etype", ALL)
+def test_ldg_driver_parity(ctx_ldg, etype):
+    n = 300_007
+    for cat, s in sorted(CATALOG.items()):
+        prog = P(s)
+        if not legal(prog, etype):
+            continue
+        ops = make_inputs(etype, n, n_operands(prog))
+        sc = SCAL[etype][:n_scalars(prog)]
+        want = oracle.eval_program(etype, prog, ops, sc)
+        r, got = run_reduce(ctx_ldg, etype, prog, ops, sc, "ACCU", with_out=True)
+        assert_elementwise(got, want, etype, max_ulp=2 if has_transcendental(prog) else 0)
+        assert_reduction(r, oracle_reduce(etype, "ACCU", want), etype, "ACCU", abs_scale(want))
+    rng = random.Random(77)
+    for trial in range(10):
+        prog = random_program(rng, 3, etype, n_ops=3)
+        ops = make_inputs(etype, 4001, n_operands(prog), seed=trial)
+        want = oracle.eval_program(etype, prog, ops, SCAL[etype][:2])
+        got = run_eval(ctx_ldg, etype, prog, ops, SCAL[etype][:2])
+        if etype == "f64" and has_transcendental(prog):
+            continue
+        assert_elementwise(got, want, etype, max_ulp=2 if has_transcendental(prog) else 0)
