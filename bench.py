@@ -166,6 +166,69 @@ def run_reference(args):
     return 0
 
 
+# The other BASELINE.json configurations (and the north-star 2^30 forms), timed
+# at N=1 after the headline: (name, elem, n_rows, n_cols, program, scalars,
+# reduce kind or None, Z stored?, algorithmic bytes per element).  Informational
+# lines beside the contract line; parity for each is in tests/test_gpu_configs.py.
+OTHER_CONFIGS = [
+    ("c1 axpy y=2.5x+y in place + accu, f32 n=1e6", "f32", 1_000_000, 1,
+     [("SCALAR", 0), ("LOAD", 0), ("MUL", 0), ("LOAD", 1), ("ADD", 0)], [2.5], "ACCU", "inplace", 12),
+    ("c2 reduce-only accu(exp(A%B)+3C), 1e4x1e4 f32", "f32", 10_000, 10_000, PROGRAM, SCALARS,
+     "ACCU", None, 12),
+    ("c3 sum(X,0), 32768^2 f64", "f64", 32768, 32768, [("LOAD", 0)], [], "SUM_DIM0", None, 8),
+    ("c3 sum(X,1), 32768^2 f64", "f64", 32768, 32768, [("LOAD", 0)], [], "SUM_DIM1", None, 8),
+    ("c4 minmax(X%Y+7Z), u32 2^28", "u32", 1 << 28, 1,
+     [("LOAD", 0), ("LOAD", 1), ("MUL", 0), ("SCALAR", 0), ("LOAD", 2), ("MUL", 0), ("ADD", 0)],
+     [7], "MINMAX", None, 12),
+    ("c4 minmax(X%Y+7Z), s64 2^28", "s64", 1 << 28, 1,
+     [("LOAD", 0), ("LOAD", 1), ("MUL", 0), ("SCALAR", 0), ("LOAD", 2), ("MUL", 0), ("ADD", 0)],
+     [7], "MINMAX", None, 24),
+    ("c5 dot(x,y), f32 2^32", "f32", 1 << 32, 1, [("LOAD", 0), ("LOAD", 1), ("MUL", 0)], [],
+     "ACCU", None, 8),
+    ("c5 norm2(x), f32 2^32", "f32", 1 << 32, 1, [("LOAD", 0)], [], "NORM2", None, 4),
+    ("headline accu(exp(A%B)+3C), f32 2^30", "f32", 1 << 30, 1, PROGRAM, SCALARS, "ACCU", None, 12),
+    ("headline exp(A%B)+3C stored + accu, f32 2^30", "f32", 1 << 30, 1, PROGRAM, SCALARS, "ACCU",
+     "out", 16),
+    ("headline y=2.5x+y in place + accu, f32 2^30", "f32", 1 << 30, 1,
+     [("SCALAR", 0), ("LOAD", 0), ("MUL", 0), ("LOAD", 1), ("ADD", 0)], [2.5], "ACCU", "inplace", 12),
+]
+
+
+def measure_other_configs(coot, ctx, peak, reps=10):
+    import torch
+    from paper_2508_11385_b200.api import TORCH_DTYPE
+    out = []
+    for name, elem, m, n, prog, sc, kind, store, bpe in OTHER_CONFIGS:
+        k = 1 + max(a for o, a in prog if o == "LOAD")
+        ops = [torch.empty(m * n, dtype=TORCH_DTYPE[elem], device="cuda") for _ in range(k)]
+        for s, t in enumerate(ops):
+            ctx.fill(t, "randu", stream=s, n_rows=m)
+        z = ops[1] if store == "inplace" else (
+            torch.empty(m * n, dtype=TORCH_DTYPE[elem], device="cuda") if store == "out" else None)
+        rlen = n if kind == "SUM_DIM0" else (m if kind == "SUM_DIM1" else 2)
+        res = torch.empty(rlen, dtype=TORCH_DTYPE[elem], device="cuda")
+
+        def call():
+            ctx.reduce(elem, m, n, prog, ops, sc, kind, res, z)
+
+        for _ in range(3):
+            call()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            call()
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / reps
+        gbs = m * n * bpe / (ms * 1e-3) / 1e9
+        out.append({"config": name, "ms": ms, "GBps": gbs, "elements_per_s": m * n / (ms * 1e-3),
+                    "frac_of_peak": gbs / peak, "path": ctx.stats()["last_path"]})
+        del ops, z, res
+        torch.cuda.empty_cache()
+    return out
+
+
 def cpu_baseline_oracle():
     """The oracle timed on this host on the full c2 workload (1e8 elements),
     single-threaded; input generation untimed.  Returns (record, accu)."""
@@ -193,6 +256,7 @@ def main():
     ap.add_argument("--impl", default="coot", choices=["coot", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-other-configs", action="store_true")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -348,10 +412,15 @@ def main():
 
     cpu = None
     parity = None
+    others = None
     if world == 1 and not args.no_cpu_baseline:
         cpu, ref_accu = cpu_baseline_oracle()
         parity = {"accu": accu, "oracle_accu": ref_accu,
                   "rel_err": abs(accu - ref_accu) / abs(ref_accu)}
+    if world == 1 and not args.no_other_configs:
+        del data, A, B, C, Z
+        torch.cuda.empty_cache()
+        others = measure_other_configs(coot, ctx, peak)
 
     alg_bytes = n * BYTES_PER_ELEM
     achieved = alg_bytes / (kern_ms * 1e-3) / 1e9
@@ -385,6 +454,7 @@ def main():
         "variants": {"reduce_only_GBps": n * 12 / (ro_ms * 1e-3) / 1e9,
                      "reduce_only_ms": ro_ms},
         "parity": parity,
+        "other_configs": others,
     }
     print(json.dumps(line), flush=True)
     if world > 1:
