@@ -18,8 +18,10 @@
  *
  * Conventions (every call)
  *   - All data pointers (operands, out, result, partials) are CUDA device
- *     pointers on the ctx's device.  Matrices are dense column-major with
- *     leading dimension n_rows (R2); Col = n x 1, Row = 1 x n.
+ *     pointers on the ctx's device.  Matrices are column-major (R2); Col =
+ *     n x 1, Row = 1 x n.  Operands may be strided views
+ *     (coot_operand.ld / .inc); `out` of coot_eval / coot_reduce and every
+ *     result are dense (coot_eval_view writes into a view).
  *   - The caller owns every data buffer; libcoot never allocates user-visible
  *     memory.  A ctx owns its scratch (reduction records, tickets), allocated
  *     in coot_init / grown on first need, freed in coot_destroy.
@@ -96,13 +98,21 @@ typedef union {
   uint64_t bits;
 } coot_scalar;
 
-/* One dense operand.  n_rows/n_cols must equal the expression's (eGlue
- * "same dimensions") else COOT_ERR_CONFORM.  ld = leading dimension in
- * elements; 0 means n_rows.  ABI v1 requires ld == n_rows (contiguous). */
+/* One operand: a dense matrix or a VIEW of one (diagonal / submatrix / row /
+ * column views, P:177 `Z.diag() += 100`).  Element (i, j) lives at
+ * ptr[i * inc + j * ld] (elements, not bytes).  n_rows/n_cols must equal the
+ * expression's (eGlue "same dimensions") else COOT_ERR_CONFORM.
+ *   ld  = elements between consecutive columns; 0 means n_rows.
+ *   inc = elements between consecutive rows;    0 means 1.
+ * A dense column-major matrix has ld = n_rows, inc = 1.  A submatrix view has
+ * ld = parent's n_rows; a diagonal view is an n x 1 Col with inc = ld + 1; a
+ * row view is 1 x n with ld = parent's n_rows.  Views that are not contiguous
+ * take a strided kernel (slower than the streaming path). */
 typedef struct {
   const void* ptr;
   uint64_t n_rows, n_cols;
   uint64_t ld;
+  uint64_t inc;
 } coot_operand;
 
 /* The expression descriptor: the runtime encoding of the compound expression
@@ -156,6 +166,14 @@ coot_status coot_validate(const coot_expr* e);
  * `out` may equal an operand pointer exactly (B += 3*A); any other
  * overlap with an operand is COOT_ERR_CONTRACT. */
 coot_status coot_eval(coot_ctx* ctx, const coot_expr* e, void* out);
+
+/* Assignment into a VIEW: out(i, j) = expr(i, j) for the view `out` (same
+ * dims as the expression), e.g. `Z.diag() += 100` is coot_eval_view with
+ * out = the diagonal view and the program [L0 S0 ADD] over that same view.
+ * The out view must not overlap itself (inc >= 1, and ld >= (n_rows-1)*inc+1
+ * when n_cols > 1); it may be IDENTICAL to an operand view (in-place update);
+ * any other overlap with an operand's address range is COOT_ERR_CONTRACT. */
+coot_status coot_eval_view(coot_ctx* ctx, const coot_expr* e, const coot_operand* out);
 
 /* result <- reduce(kind, expr), in one launch.  If out_or_null is non-NULL
  * the element-wise result is also written in the same pass ("Z = ...; then

@@ -41,7 +41,17 @@ class Scalar(ctypes.Union):
 
 class Operand(ctypes.Structure):
     _fields_ = [("ptr", ctypes.c_void_p), ("n_rows", ctypes.c_uint64),
-                ("n_cols", ctypes.c_uint64), ("ld", ctypes.c_uint64)]
+                ("n_cols", ctypes.c_uint64), ("ld", ctypes.c_uint64), ("inc", ctypes.c_uint64)]
+
+
+def make_operand(o) -> Operand:
+    """(ptr, n_rows, n_cols[, ld, inc]) -> coot_operand (ld/inc 0 = dense)."""
+    op = Operand()
+    op.ptr = o[0]
+    op.n_rows, op.n_cols = o[1], o[2]
+    op.ld = o[3] if len(o) > 3 else 0
+    op.inc = o[4] if len(o) > 4 else 0
+    return op
 
 
 class Expr(ctypes.Structure):
@@ -78,6 +88,7 @@ _SIGS = {
     "coot_destroy": (_i32, [_vp]),
     "coot_set_stream": (_i32, [_vp, _vp]),
     "coot_eval": (_i32, [_vp, ctypes.POINTER(Expr), _vp]),
+    "coot_eval_view": (_i32, [_vp, ctypes.POINTER(Expr), ctypes.POINTER(Operand)]),
     "coot_reduce": (_i32, [_vp, ctypes.POINTER(Expr), _u32, _vp, _vp]),
     "coot_reduce_partial": (_i32, [_vp, ctypes.POINTER(Expr), _u32, _vp, _vp]),
     "coot_combine": (_i32, [_vp, _u32, _u32, _vp, _u32, _u64, _vp]),
@@ -134,14 +145,9 @@ def make_expr(elem: str, n_rows: int, n_cols: int, program, operands, scalars=()
     e.n_scalars = len(scalars)
     e.n_instr = len(program)
     for k, o in enumerate(operands[:MAX_OPERANDS]):
-        if isinstance(o, tuple):
-            ptr, r, c = o
-        else:
-            ptr, r, c = o.data_ptr(), n_rows, n_cols
-        e.operands[k].ptr = ptr
-        e.operands[k].n_rows = r
-        e.operands[k].n_cols = c
-        e.operands[k].ld = 0
+        if not isinstance(o, tuple):
+            o = (o.data_ptr(), n_rows, n_cols)
+        e.operands[k] = make_operand(o)
     for k, s in enumerate(list(scalars)[:MAX_SCALARS]):
         set_scalar(e.scalars[k], elem, s)
     for i, (op, arg) in enumerate(list(program)[:MAX_INSTR]):

@@ -83,6 +83,12 @@ class Context:
         e = N.make_expr(elem, n_rows, n_cols, program, operands, scalars)
         check(lib.coot_eval(self.handle, ctypes.byref(e), ctypes.c_void_p(out.data_ptr())))
 
+    def eval_view(self, elem, n_rows, n_cols, program, operands, scalars, out: tuple):
+        """Assign into a strided destination view (ptr, n_rows, n_cols, ld, inc)."""
+        e = N.make_expr(elem, n_rows, n_cols, program, operands, scalars)
+        o = N.make_operand(out)
+        check(lib.coot_eval_view(self.handle, ctypes.byref(e), ctypes.byref(o)))
+
     def reduce(self, elem, n_rows, n_cols, program, operands, scalars, kind,
                result: torch.Tensor, out: torch.Tensor | None = None):
         e = N.make_expr(elem, n_rows, n_cols, program, operands, scalars)
@@ -207,8 +213,8 @@ class Expr:
         return self.n_rows * self.n_cols
 
     # ---- evaluation ------------------------------------------------------
-    def eval(self, ctx: Context | None = None, out: "Mat | None" = None) -> "Mat":
-        """Assign the expression to a (new or given) matrix: ONE launch."""
+    def eval(self, ctx: Context | None = None, out: "Mat | View | None" = None):
+        """Assign the expression to a (new or given) matrix or view: ONE launch."""
         lw = lower(self)
         ctx = ctx or default_ctx(lw.device_index())
         if out is None:
@@ -216,7 +222,11 @@ class Expr:
         elif (out.n_rows, out.n_cols, out.elem) != (lw.n_rows, lw.n_cols, lw.elem):
             raise CootError(2, f"conformability: assignment target is {out.n_rows}x{out.n_cols} "
                                f"{out.elem}, expression is {lw.n_rows}x{lw.n_cols} {lw.elem}")
-        ctx.eval(lw.elem, lw.n_rows, lw.n_cols, lw.program, lw.operands, lw.scalars, out.data)
+        if isinstance(out, View):
+            ctx.eval_view(lw.elem, lw.n_rows, lw.n_cols, lw.program, lw.operands, lw.scalars,
+                          out.operand())
+        else:
+            ctx.eval(lw.elem, lw.n_rows, lw.n_cols, lw.program, lw.operands, lw.scalars, out.data)
         return out
 
 
@@ -267,9 +277,81 @@ class Mat(Expr):
         """(rows x cols) row-major view copy of the column-major data."""
         return self.data.reshape(self.n_cols, self.n_rows).t()
 
+    # ---- views (P:177 `Z.diag() += 100`, P:255 diagonal / submatrix views) -----
+    def diag(self, k: int = 0) -> "View":
+        """k-th diagonal as an n x 1 Col view (k > 0 above, k < 0 below the main)."""
+        m, n = self.n_rows, self.n_cols
+        if k >= 0:
+            length, off = max(0, min(m, n - k)), k * m
+        else:
+            length, off = max(0, min(m + k, n)), -k
+        if length == 0:
+            raise CootError(3, f"bounds: diagonal {k} of a {m}x{n} matrix is empty")
+        return View(self, off, length, 1, ld=length, inc=m + 1)
+
+    def submat(self, r0: int, c0: int, r1: int, c1: int) -> "View":
+        """Rows r0..r1, columns c0..c1 (inclusive, Armadillo convention)."""
+        if not (0 <= r0 <= r1 < self.n_rows and 0 <= c0 <= c1 < self.n_cols):
+            raise CootError(3, f"bounds: submat({r0},{c0},{r1},{c1}) of {self.n_rows}x{self.n_cols}")
+        return View(self, r0 + c0 * self.n_rows, r1 - r0 + 1, c1 - c0 + 1, ld=self.n_rows, inc=1)
+
+    def col(self, j: int) -> "View":
+        return self.submat(0, j, self.n_rows - 1, j)
+
+    def row(self, i: int) -> "View":
+        return self.submat(i, 0, i, self.n_cols - 1)
+
+    def operand(self) -> tuple:
+        return (self.data.data_ptr(), self.n_rows, self.n_cols, self.n_rows, 1)
+
     def assign(self, e: Expr, ctx: Context | None = None) -> "Mat":
         """self = e (exact aliasing with an operand is allowed: B += 3*A)."""
         return as_expr(e, self.elem).eval(ctx, out=self)
+
+    def __iadd__(self, o):
+        return self.assign(self + o)
+
+    def __isub__(self, o):
+        return self.assign(self - o)
+
+    def __imod__(self, o):
+        return self.assign(self % o)
+
+    def __imul__(self, o):
+        return self.assign(self * o)
+
+    def __itruediv__(self, o):
+        return self.assign(self / o)
+
+
+class View(Expr):
+    """A strided view of a Mat: element (i, j) at parent.data[offset + i*inc + j*ld].
+    Usable as an operand anywhere, and as an assignment target (`d = Z.diag();
+    d += 100` evaluates [L0 S0 ADD] into the diagonal in one launch)."""
+
+    def __init__(self, parent: Mat, offset: int, n_rows: int, n_cols: int, ld: int, inc: int):
+        self.parent = parent
+        self.offset = int(offset)
+        self.n_rows, self.n_cols = int(n_rows), int(n_cols)
+        self.ld, self.inc = int(ld), int(inc)
+        self.elem = parent.elem
+
+    @property
+    def data(self):
+        raise CootError(5, "contract: a View has no dense storage; use to_torch()")
+
+    def operand(self) -> tuple:
+        ptr = self.parent.data.data_ptr() + self.offset * ESIZE[self.elem]
+        return (ptr, self.n_rows, self.n_cols, self.ld, self.inc)
+
+    def to_torch(self) -> torch.Tensor:
+        """(rows x cols) copy of the viewed elements."""
+        t = torch.as_strided(self.parent.data, (self.n_cols, self.n_rows), (self.ld, self.inc),
+                             self.offset)
+        return t.t().contiguous()
+
+    def assign(self, e: Expr, ctx: Context | None = None) -> "View":
+        return as_expr(e).eval(ctx, out=self)
 
     def __iadd__(self, o):
         return self.assign(self + o)
@@ -346,15 +428,19 @@ def square(x): return _unary("SQUARE", x)
 
 
 class Lowered:
-    def __init__(self, elem, n_rows, n_cols, program, operands, scalars):
+    """A lowered expression: postfix program + operands (dense tensors or view
+    tuples (ptr, n_rows, n_cols, ld, inc)) + scalars."""
+
+    def __init__(self, elem, n_rows, n_cols, program, operands, scalars, dev=None):
         self.elem, self.n_rows, self.n_cols = elem, n_rows, n_cols
         self.program, self.operands, self.scalars = program, operands, scalars
+        self.dev = dev
 
     def device(self):
-        return self.operands[0].device
+        return self.dev
 
     def device_index(self):
-        return self.operands[0].device.index
+        return self.dev.index
 
 
 def lower(e: Expr) -> Lowered:
@@ -362,21 +448,23 @@ def lower(e: Expr) -> Lowered:
     storage (each distinct array is loaded once); scalars by value."""
     if isinstance(e, ScalarLeaf):
         raise TypeError("scalar-only expression")
-    operands: list[torch.Tensor] = []
-    op_index: dict[int, int] = {}
+    operands: list = []
+    op_index: dict = {}
     scalars: list = []
     program: list[tuple[str, int]] = []
     elem, nr, nc = e.elem, e.n_rows, e.n_cols
+    dev = [None]
 
     def visit(x):
-        if isinstance(x, Mat):
+        if isinstance(x, (Mat, View)):
             if (x.n_rows, x.n_cols) != (nr, nc):
                 raise CootError(2, f"conformability: operand is {x.n_rows}x{x.n_cols}, "
                                    f"expression is {nr}x{nc}")
-            key = x.data.data_ptr()
+            key = x.operand()
             if key not in op_index:
                 op_index[key] = len(operands)
-                operands.append(x.data)
+                operands.append(x.data if isinstance(x, Mat) else key)
+                dev[0] = dev[0] or (x.data.device if isinstance(x, Mat) else x.parent.data.device)
             program.append(("LOAD", op_index[key]))
         elif isinstance(x, ScalarLeaf):
             v = x.value
@@ -398,7 +486,7 @@ def lower(e: Expr) -> Lowered:
             program.append((x.op, 0))
 
     visit(e)
-    return Lowered(elem, nr, nc, program, operands, scalars)
+    return Lowered(elem, nr, nc, program, operands, scalars, dev[0])
 
 
 # ---- terminal reductions ----------------------------------------------------

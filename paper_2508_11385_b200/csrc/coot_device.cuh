@@ -54,6 +54,10 @@ struct FusedArgs {
   uint32_t n_instr;
   uint32_t tile_units;  // TMA driver: 16-byte units per tile (multiple of 256)
   uint32_t stages;      // TMA driver: smem pipeline depth
+  // strided (view) path: element (i, j) of operand k at in[k][i*inc[k] + j*ld[k]]
+  u64 m;                // rows of the expression
+  u64 ld[COOT_MAX_OPERANDS], inc[COOT_MAX_OPERANDS];
+  u64 out_ld, out_inc;
   uint16_t key[COOT_MAX_INSTR];  // interpreter dispatch index: op * 9 + depth
   uint8_t arg[COOT_MAX_INSTR];
 };

@@ -29,6 +29,7 @@ struct DimArgs {
   uint32_t nchunks;     // dim1: column chunks (1 = no split)
   uint32_t nrt;         // dim1: row tiles
   uint32_t cg;          // dim1 TMA: columns per pipeline stage
+  uint32_t dim;         // strided kernel: 0 or 1
 };
 
 template <class T>
@@ -144,6 +145,54 @@ __global__ void __launch_bounds__(kThreads) dim0_warp_kernel(const __grid_consta
     }
     acc.warp_reduce();
     if (lane == 0) store_dim_value<T>(d, j, acc.s);
+  }
+}
+
+// ---- strided views: sum(view, 0) warp per column, sum(view, 1) thread per row --
+// Operand k element (i, j) at in[k][i*inc[k] + j*ld[k]] (d.f.ld / d.f.inc).
+template <class T, class EV>
+__device__ __forceinline__ void load_elem_strided(const FusedArgs& a, u64 i, u64 j,
+                                                  T (&in)[EV::K][1]) {
+#pragma unroll
+  for (int k = 0; k < EV::K; ++k) {
+    if (!EV::kInterp || k < (int)a.n_operands)
+      in[k][0] = __ldcg(reinterpret_cast<const T*>(a.in[k]) + i * a.inc[k] + j * a.ld[k]);
+    else
+      in[k][0] = T(0);
+  }
+}
+
+template <class T, class EV>
+__global__ void __launch_bounds__(kThreads) dim_strided_kernel(const __grid_constant__ DimArgs d) {
+  if (d.dim == 0) {
+    const int lane = threadIdx.x & 31;
+    const u64 warp = ((u64)blockIdx.x * kThreads + threadIdx.x) >> 5;
+    const u64 nwarps = ((u64)gridDim.x * kThreads) >> 5;
+    for (u64 j = warp; j < d.n; j += nwarps) {
+      Accum<T, ACC_SUM> acc;
+      acc.init();
+      for (u64 i = lane; i < d.m; i += 32) {
+        T in[EV::K][1], v[1];
+        load_elem_strided<T, EV>(d.f, i, j, in);
+        EV::template eval<T, 1>(in, d.f, v);
+        acc.template add<1>(v);
+      }
+      acc.warp_reduce();
+      if (lane == 0) store_dim_value<T>(d, j, acc.s);
+    }
+  } else {
+    for (u64 i = (u64)blockIdx.x * kThreads + threadIdx.x; i < d.m;
+         i += (u64)gridDim.x * kThreads) {
+      Accum<T, ACC_SUM> acc;
+      acc.init();
+      for (u64 j = 0; j < d.n; ++j) {
+        T in[EV::K][1], v[1];
+        load_elem_strided<T, EV>(d.f, i, j, in);
+        EV::template eval<T, 1>(in, d.f, v);
+        acc.template add<1>(v);
+      }
+      store_dim_value<T>(d, i, acc.s);
+    }
   }
 }
 

@@ -326,6 +326,49 @@ __global__ void __launch_bounds__(kThreads, EV::kInterp ? 1 : COOT_CAT_MINB)
   }
 }
 
+// ---- strided driver (views: diag / submatrix / row) -------------
+// Element e of the m x n expression -> (i, j) = (e mod m, e / m); operand k
+// is read at in[k][i*inc[k] + j*ld[k]] and the result written to
+// out[i*out_inc + j*out_ld].  Thread t walks e = t, t + N, ... (N threads);
+// (i, j) advance incrementally, no division in the loop.  Always driven by the
+// interpreter (one kernel per type/reduction), so results do not depend on
+// catalog matching.
+template <class T, int ACC, class EV>
+__global__ void __launch_bounds__(kThreads) fused_strided_kernel(const __grid_constant__ FusedArgs a) {
+  constexpr int K = EV::K;
+  Accum<T, ACC> acc;
+  acc.init();
+  const u64 tid = (u64)blockIdx.x * kThreads + threadIdx.x;
+  const u64 nthr = (u64)gridDim.x * kThreads;
+  const u64 m = a.m;
+  u64 i = tid % m, j = tid / m;
+  const u64 di = nthr % m, dj = nthr / m;
+  T* out = reinterpret_cast<T*>(a.out);
+  for (u64 e = tid; e < a.n; e += nthr) {
+    T in[K][1], v[1];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      if (!EV::kInterp || k < (int)a.n_operands)
+        in[k][0] = __ldcg(reinterpret_cast<const T*>(a.in[k]) + i * a.inc[k] + j * a.ld[k]);
+      else
+        in[k][0] = T(0);
+    }
+    EV::template eval<T, 1>(in, a, v);
+    if (out) out[i * a.out_inc + j * a.out_ld] = v[0];
+    acc.template add<1>(v);
+    i += di;
+    j += dj;
+    if (i >= m) {
+      i -= m;
+      ++j;
+    }
+  }
+  if constexpr (ACC != ACC_NONE) {
+    Accum<T, ACC> bt = block_reduce<T, ACC>(acc);
+    grid_finish<T, ACC>(bt, a.partials, a.ticket, a.final_mode, a.kind, a.result, a.count);
+  }
+}
+
 // ---- the TMA-staged driver (default on B200) ---------------------------------
 // One producer warp streams tiles of every operand into a `stages`-deep shared
 // memory ring with 1-D bulk copies (cp.async.bulk + mbarrier complete_tx,

@@ -20,7 +20,8 @@ struct FusedPlan {
 
 enum DimKernel {
   DIMK_DIM0_BLOCK = 0, DIMK_DIM0_WARP = 1, DIMK_DIM1 = 2,  // LDG kernels
-  DIMK_DIM0_TMA = 3, DIMK_DIM1_TMA = 4                     // TMA-staged kernels
+  DIMK_DIM0_TMA = 3, DIMK_DIM1_TMA = 4,                    // TMA-staged kernels
+  DIMK_STRIDED = 5                                         // strided views
 };
 
 struct DimPlan {

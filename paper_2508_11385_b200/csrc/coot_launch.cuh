@@ -17,8 +17,12 @@ typedef void (*DimFn)(const DimArgs);
 // ahead) so every thread keeps >= 64 bytes of loads in flight.
 constexpr int unroll_for(int k) { return k <= 1 ? 4 : (k == 2 ? 2 : 1); }
 
+// driver: 0 = LDG, 1 = TMA-staged, 2 = strided views (interpreter only)
 template <class T, int ACC, class EV, int U>
 FusedFn driver_kernel(int driver) {
+  if constexpr (EV::kInterp) {
+    if (driver == 2) return &fused_strided_kernel<T, ACC, EV>;
+  }
   if (driver == 1) return &fused_tma_kernel<T, ACC, EV>;
   return &fused_kernel<T, ACC, EV, U>;
 }
@@ -26,6 +30,7 @@ FusedFn driver_kernel(int driver) {
 template <class T, int ACC, int... Code>
 FusedFn catalog_kernel(int driver) {
   typedef StaticProg<Code...> P;
+  if (driver == 2) return nullptr;  // views always run on the interpreter
   if constexpr (P::template legal<T>()) {
     return driver_kernel<T, ACC, CatalogEval<P>, unroll_for(P::n_ops())>(driver);
   } else {
@@ -110,6 +115,10 @@ struct Dim1 {
   static constexpr DimFn run = &dim1_kernel<T, EV>;
 };
 template <class T, class EV>
+struct DimStrided {
+  static constexpr DimFn run = &dim_strided_kernel<T, EV>;
+};
+template <class T, class EV>
 struct Dim0Tma {
   static constexpr DimFn run = &dim0_tma_kernel<T, EV>;
 };
@@ -128,6 +137,7 @@ cudaError_t launch_dim_t(const DimPlan& p, const DimArgs& a, cudaStream_t s) {
     case DIMK_DIM1: k = pick_dim_ev<T, Dim1>(p); break;
     case DIMK_DIM0_TMA: k = pick_dim_ev<T, Dim0Tma>(p); tma = true; break;
     case DIMK_DIM1_TMA: k = pick_dim_ev<T, Dim1Tma>(p); tma = true; break;
+    case DIMK_STRIDED: k = pick_dim_ev<T, DimStrided>(p); break;
   }
   if (!k) return cudaErrorInvalidDeviceFunction;
   if (tma) {

@@ -120,11 +120,7 @@ coot_status validate_expr(const coot_expr* e, Shape* shape) {
   const size_t es = elem_size(e->elem);
   for (uint32_t k = 0; k < e->n_operands; ++k) {
     const coot_operand& o = e->operands[k];
-    if (o.ld != 0 && o.ld != o.n_rows)
-      return fail(COOT_ERR_CONTRACT,
-                  "contract: operand %u has leading dimension %llu != n_rows %llu "
-                  "(strided views are not supported by ABI v1)",
-                  k, (unsigned long long)o.ld, (unsigned long long)o.n_rows);
+    // any (ld, inc) is a legal READ view; only written views must not overlap themselves
     if (n > 0 && o.ptr == nullptr)
       return fail(COOT_ERR_CONTRACT, "contract: operand %u is NULL with %llu elements", k,
                   (unsigned long long)n);
@@ -190,26 +186,61 @@ bool ranges_overlap(uintptr_t a, size_t na, uintptr_t b, size_t nb) {
   return a < b + nb && b < a + na;
 }
 
-// out may equal an operand exactly (B += 3*A); any other overlap is an error.
-coot_status check_out_alias(const coot_expr* e, const void* out, size_t bytes) {
-  if (!out) return ok();
-  const uintptr_t o = reinterpret_cast<uintptr_t>(out);
+// ---- views (coot_operand.ld / .inc) ------------------------------------------
+u64 op_ld(const coot_operand& o) { return o.ld ? o.ld : o.n_rows; }
+u64 op_inc(const coot_operand& o) { return o.inc ? o.inc : 1; }
+bool op_dense(const coot_operand& o) {
+  return op_inc(o) == 1 && (o.n_cols <= 1 || op_ld(o) == o.n_rows);
+}
+// Bytes from the view's first element to one past its last element.
+size_t op_span_bytes(const coot_operand& o, size_t es) {
+  if (o.n_rows == 0 || o.n_cols == 0) return 0;
+  return (size_t)(((o.n_rows - 1) * op_inc(o) + (o.n_cols - 1) * op_ld(o) + 1) * es);
+}
+bool same_view(const coot_operand& a, const coot_operand& b) {
+  return a.ptr == b.ptr && a.n_rows == b.n_rows && a.n_cols == b.n_cols && op_ld(a) == op_ld(b) &&
+         op_inc(a) == op_inc(b);
+}
+coot_operand dense_view(const void* p, u64 m, u64 n) {
+  coot_operand o;
+  o.ptr = p;
+  o.n_rows = m;
+  o.n_cols = n;
+  o.ld = m;
+  o.inc = 1;
+  return o;
+}
+
+// out may be IDENTICAL to an operand view (B += 3*A; Z.diag() += 100,
+// P:177); any other overlap of address spans is an error.  A written view
+// must not overlap itself.
+coot_status check_out_alias(const coot_expr* e, const coot_operand* out) {
+  if (!out || !out->ptr) return ok();
+  const size_t es = elem_size(e->elem);
+  if (out->n_cols > 1 && op_ld(*out) < (out->n_rows ? (out->n_rows - 1) * op_inc(*out) + 1 : 0))
+    return fail(COOT_ERR_CONTRACT, "contract: out view overlaps itself (ld %llu < (n_rows-1)*inc+1)",
+                (unsigned long long)op_ld(*out));
+  const uintptr_t o = reinterpret_cast<uintptr_t>(out->ptr);
+  const size_t ob = op_span_bytes(*out, es);
   for (uint32_t k = 0; k < e->n_operands; ++k) {
-    const uintptr_t p = reinterpret_cast<uintptr_t>(e->operands[k].ptr);
-    if (p == o) continue;
-    if (ranges_overlap(o, bytes, p, bytes))
+    if (same_view(*out, e->operands[k])) continue;
+    if (ranges_overlap(o, ob, reinterpret_cast<uintptr_t>(e->operands[k].ptr),
+                       op_span_bytes(e->operands[k], es)))
       return fail(COOT_ERR_CONTRACT, "contract: out partially overlaps operand %u (only exact aliasing is allowed)", k);
   }
   return ok();
 }
 
 coot_status check_result_alias(const coot_expr* e, const void* result, size_t rbytes,
-                               const void* out, size_t bytes) {
+                               const coot_operand* out) {
+  const size_t es = elem_size(e->elem);
   const uintptr_t r = reinterpret_cast<uintptr_t>(result);
   for (uint32_t k = 0; k < e->n_operands; ++k)
-    if (ranges_overlap(r, rbytes, reinterpret_cast<uintptr_t>(e->operands[k].ptr), bytes))
+    if (ranges_overlap(r, rbytes, reinterpret_cast<uintptr_t>(e->operands[k].ptr),
+                       op_span_bytes(e->operands[k], es)))
       return fail(COOT_ERR_CONTRACT, "contract: result overlaps operand %u", k);
-  if (out && ranges_overlap(r, rbytes, reinterpret_cast<uintptr_t>(out), bytes))
+  if (out && out->ptr &&
+      ranges_overlap(r, rbytes, reinterpret_cast<uintptr_t>(out->ptr), op_span_bytes(*out, es)))
     return fail(COOT_ERR_CONTRACT, "contract: result overlaps out");
   return ok();
 }
@@ -268,6 +299,11 @@ void fill_program(const coot_expr* e, coot::FusedArgs* a) {
     a->scalars[s] = s < e->n_scalars ? e->scalars[s].bits : 0;
   a->n_operands = e->n_operands;
   a->n_instr = e->n_instr;
+  a->m = e->n_rows;
+  for (uint32_t k = 0; k < COOT_MAX_OPERANDS; ++k) {
+    a->ld[k] = k < e->n_operands ? op_ld(e->operands[k]) : 0;
+    a->inc[k] = k < e->n_operands ? op_inc(e->operands[k]) : 0;
+  }
   int sp = 0;
   for (uint32_t i = 0; i < e->n_instr; ++i) {
     const int op = e->prog[i].op, arg = e->prog[i].arg;
@@ -366,9 +402,55 @@ u64 alg_bytes(const coot_expr* e, const Shape& sh, bool store) {
   return n * elem_size(e->elem) * k;
 }
 
+bool any_strided(const coot_expr* e, const coot_operand* outv) {
+  bool s = outv && outv->ptr && !op_dense(*outv);
+  for (uint32_t k = 0; k < e->n_operands; ++k) s = s || !op_dense(e->operands[k]);
+  return s;
+}
+
+// Views: the strided kernel (interpreter), element (i, j) addressed per operand.
+coot_status run_strided(coot_ctx* ctx, const coot_expr* e, const Shape& sh, int acc,
+                        uint32_t kind, void* result, uint32_t final_mode,
+                        const coot_operand* outv) {
+  const u64 n = e->n_rows * e->n_cols;
+  coot::FusedArgs a;
+  memset(&a, 0, sizeof a);
+  fill_program(e, &a);
+  a.n = n;
+  a.out = outv ? const_cast<void*>(outv->ptr) : nullptr;
+  a.out_ld = outv ? op_ld(*outv) : 0;
+  a.out_inc = outv ? op_inc(*outv) : 0;
+  a.partials = ctx->recs;
+  a.ticket = ctx->ticket;
+  a.result = result;
+  a.count = n;
+  a.final_mode = final_mode;
+  a.kind = kind;
+  coot::FusedPlan p;
+  p.driver = 2;
+  p.smem = 0;
+  p.catalog = -1;
+  p.interp_large = (e->n_operands > 4 || sh.max_depth > 4) ? 1 : 0;
+  p.acc = acc;
+  p.grid = (unsigned)std::max<u64>(
+      1, std::min<u64>(ceil_div(n, coot::kThreads), (u64)ctx->sm_count * ctx->blocks_per_sm));
+  if (ctx->log)
+    fprintf(stderr, "[coot] strided elem=%u %llux%llu acc=%d grid=%u\n", e->elem,
+            (unsigned long long)e->n_rows, (unsigned long long)e->n_cols, acc, p.grid);
+  cudaError_t ce = dispatch_fused(e->elem, p, a, ctx->stream);
+  if (ce != cudaSuccess) return cuda_fail(ce, "strided kernel launch");
+  ctx->stats.launches++;
+  ctx->stats.last_path = -4;
+  ctx->stats.last_grid = p.grid;
+  ctx->stats.last_alg_bytes = alg_bytes(e, sh, a.out != nullptr);
+  return ok();
+}
+
 // The fused pass (eval / full reductions).
 coot_status run_fused(coot_ctx* ctx, const coot_expr* e, const Shape& sh, int acc, uint32_t kind,
-                      void* result, uint32_t final_mode, void* out) {
+                      void* result, uint32_t final_mode, const coot_operand* outv) {
+  if (any_strided(e, outv)) return run_strided(ctx, e, sh, acc, kind, result, final_mode, outv);
+  void* out = (outv && outv->ptr) ? const_cast<void*>(outv->ptr) : nullptr;
   const size_t es = elem_size(e->elem);
   const u64 n = e->n_rows * e->n_cols;
   const u64 W = 16 / es;
@@ -479,7 +561,14 @@ coot_status run_dim(coot_ctx* ctx, const coot_expr* e, const Shape& sh, uint32_t
   const u64 G = (u64)ctx->sm_count * ctx->tma_ctas_per_sm;  // TMA grid: persistent CTAs
   const u64 nk = e->n_operands;
   const u64 R1 = (u64)coot::kConsumerWarps * 32 * W;         // dim1 TMA rows per tile
-  if (kind == COOT_RED_SUM_DIM0 && use_tma && same && col_aligned && m * es >= 4096) {
+  if (any_strided(e, nullptr)) {
+    // views: warp per column (dim 0) / thread per row (dim 1), interpreter
+    p.kernel = coot::DIMK_STRIDED;
+    p.catalog = -1;
+    d.dim = kind == COOT_RED_SUM_DIM0 ? 0 : 1;
+    const u64 work = d.dim == 0 ? n * 32 : m;
+    p.grid = (unsigned)std::max<u64>(1, std::min<u64>(ceil_div(work, coot::kThreads), target));
+  } else if (kind == COOT_RED_SUM_DIM0 && use_tma && same && col_aligned && m * es >= 4096) {
     // TMA dim 0: pieces = (column, segment), ~8 pieces per CTA, segments >= 1 tile
     p.kernel = coot::DIMK_DIM0_TMA;
     d.vec_ok = 1;
@@ -611,36 +700,63 @@ coot_status reduce_common(coot_ctx* ctx, const coot_expr* e, uint32_t kind, void
   if (final_mode == coot::FINAL_ROUND && n == 0 &&
       (kind == COOT_RED_MIN || kind == COOT_RED_MAX || kind == COOT_RED_MINMAX))
     return fail(COOT_ERR_CONTRACT, "contract: min/max of an empty expression");
-  st = check_out_alias(e, out, n * es);
+  if (out && reinterpret_cast<uintptr_t>(out) % es)
+    return fail(COOT_ERR_CONTRACT, "contract: out is not aligned to its element size");
+  const coot_operand outv = dense_view(out, e->n_rows, e->n_cols);
+  st = check_out_alias(e, out ? &outv : nullptr);
   if (st != COOT_OK) return st;
   size_t rbytes = result_bytes(kind, es, e->n_rows, e->n_cols);
   if (final_mode == coot::FINAL_PARTIAL)
     rbytes = dim ? (kind == COOT_RED_SUM_DIM0 ? e->n_cols : e->n_rows) * 8 : COOT_PARTIAL_BYTES;
-  st = check_result_alias(e, result, rbytes, out, n * es);
+  st = check_result_alias(e, result, rbytes, out ? &outv : nullptr);
   if (st != COOT_OK) return st;
   st = bind_device(ctx);
   if (st != COOT_OK) return st;
-  const coot_expr ce = compact_expr(e, &sh);
-  if (dim) return run_dim(ctx, &ce, sh, kind, result, final_mode);
+  const coot_expr cx = compact_expr(e, &sh);
+  if (dim) return run_dim(ctx, &cx, sh, kind, result, final_mode);
   const int acc = acc_for_kind(kind);
   if (n == 0) {
     if (final_mode == coot::FINAL_PARTIAL) {
-      cudaError_t ce;
+      cudaError_t cerr;
       switch (e->elem) {
-        case COOT_F32: ce = coot::launch_empty_rec_t<float>(acc, result, ctx->stream); break;
-        case COOT_F64: ce = coot::launch_empty_rec_t<double>(acc, result, ctx->stream); break;
-        case COOT_U32: ce = coot::launch_empty_rec_t<uint32_t>(acc, result, ctx->stream); break;
-        default: ce = coot::launch_empty_rec_t<coot::s64>(acc, result, ctx->stream); break;
+        case COOT_F32: cerr = coot::launch_empty_rec_t<float>(acc, result, ctx->stream); break;
+        case COOT_F64: cerr = coot::launch_empty_rec_t<double>(acc, result, ctx->stream); break;
+        case COOT_U32: cerr = coot::launch_empty_rec_t<uint32_t>(acc, result, ctx->stream); break;
+        default: cerr = coot::launch_empty_rec_t<coot::s64>(acc, result, ctx->stream); break;
       }
-      if (ce != cudaSuccess) return cuda_fail(ce, "empty record launch");
+      if (cerr != cudaSuccess) return cuda_fail(cerr, "empty record launch");
       ctx->stats.launches++;
       return ok();
     }
-    cudaError_t ce = cudaMemsetAsync(result, 0, es, ctx->stream);  // ACCU / NORM2 of empty = 0
-    if (ce != cudaSuccess) return cuda_fail(ce, "cudaMemsetAsync");
+    cudaError_t cerr = cudaMemsetAsync(result, 0, es, ctx->stream);  // ACCU / NORM2 of empty = 0
+    if (cerr != cudaSuccess) return cuda_fail(cerr, "cudaMemsetAsync");
     return ok();
   }
-  return run_fused(ctx, &ce, sh, acc, kind, result, final_mode, out);
+  return run_fused(ctx, &cx, sh, acc, kind, result, final_mode, out ? &outv : nullptr);
+}
+
+// Assignment of an expression into a (dense or view) destination: one launch.
+coot_status eval_common(coot_ctx* ctx, const coot_expr* e, const coot_operand* outv) {
+  coot_status st = check_ctx(ctx);
+  if (st != COOT_OK) return st;
+  Shape sh;
+  st = validate_expr(e, &sh);
+  if (st != COOT_OK) return st;
+  const u64 n = e->n_rows * e->n_cols;
+  if (n == 0) return ok();  // zero launches for an empty expression
+  if (!outv || !outv->ptr) return fail(COOT_ERR_CONTRACT, "contract: out is NULL");
+  if (outv->n_rows != e->n_rows || outv->n_cols != e->n_cols)
+    return fail(COOT_ERR_CONFORM, "conformability: out is %llux%llu, expression is %llux%llu",
+                (unsigned long long)outv->n_rows, (unsigned long long)outv->n_cols,
+                (unsigned long long)e->n_rows, (unsigned long long)e->n_cols);
+  if (reinterpret_cast<uintptr_t>(outv->ptr) % elem_size(e->elem))
+    return fail(COOT_ERR_CONTRACT, "contract: out is not aligned to its element size");
+  st = check_out_alias(e, outv);
+  if (st != COOT_OK) return st;
+  st = bind_device(ctx);
+  if (st != COOT_OK) return st;
+  const coot_expr cx = compact_expr(e, &sh);
+  return run_fused(ctx, &cx, sh, coot::ACC_NONE, COOT_RED_ACCU, nullptr, coot::FINAL_ROUND, outv);
 }
 
 }  // namespace
@@ -747,22 +863,14 @@ coot_status coot_set_stream(coot_ctx* ctx, void* cuda_stream) {
 }
 
 coot_status coot_eval(coot_ctx* ctx, const coot_expr* e, void* out) {
-  coot_status st = check_ctx(ctx);
-  if (st != COOT_OK) return st;
-  Shape sh;
-  st = validate_expr(e, &sh);
-  if (st != COOT_OK) return st;
-  const u64 n = e->n_rows * e->n_cols;
-  if (n == 0) return ok();  // zero launches for an empty expression
-  if (!out) return fail(COOT_ERR_CONTRACT, "contract: out is NULL");
-  st = check_out_alias(e, out, n * elem_size(e->elem));
-  if (st != COOT_OK) return st;
-  if (reinterpret_cast<uintptr_t>(out) % elem_size(e->elem))
-    return fail(COOT_ERR_CONTRACT, "contract: out is not aligned to its element size");
-  st = bind_device(ctx);
-  if (st != COOT_OK) return st;
-  const coot_expr ce = compact_expr(e, &sh);
-  return run_fused(ctx, &ce, sh, coot::ACC_NONE, COOT_RED_ACCU, nullptr, coot::FINAL_ROUND, out);
+  if (!e) return fail(COOT_ERR_CONTRACT, "contract: expression descriptor is NULL");
+  const coot_operand outv = dense_view(out, e->n_rows, e->n_cols);
+  return eval_common(ctx, e, &outv);
+}
+
+coot_status coot_eval_view(coot_ctx* ctx, const coot_expr* e, const coot_operand* out) {
+  if (!out) return fail(COOT_ERR_CONTRACT, "contract: out view is NULL");
+  return eval_common(ctx, e, out);
 }
 
 coot_status coot_reduce(coot_ctx* ctx, const coot_expr* e, uint32_t kind, void* result,

@@ -108,10 +108,17 @@ def test_abi_version_mismatch_is_config_error():
     assert "abi_version" in N.lib.coot_last_error().decode()
 
 
-def test_strided_operand_rejected_in_v1():
-    e = N.make_expr("f32", 10, 10, [("LOAD", 0)], [A])
-    e.operands[0].ld = 16
-    assert N.lib.coot_validate(ctypes.byref(e)) == 5
+def test_strided_view_operands_validate():
+    # submatrix (ld > n_rows) and diagonal (inc = ld + 1) views are legal operands
+    e = N.make_expr("f32", 10, 10, [("LOAD", 0), ("LOAD", 1), ("ADD", 0)],
+                    [(1 << 20, 10, 10, 16, 1), (1 << 22, 10, 10)])
+    assert N.lib.coot_validate(ctypes.byref(e)) == 0
+    e = N.make_expr("f64", 7, 1, [("LOAD", 0), ("SCALAR", 0), ("ADD", 0)],
+                    [(1 << 20, 7, 1, 7, 8)], [100.0])
+    assert N.lib.coot_validate(ctypes.byref(e)) == 0
+    # a view whose dims disagree is still a conformability error
+    e = N.make_expr("f32", 10, 10, [("LOAD", 0)], [(1 << 20, 10, 9, 16, 1)])
+    assert N.lib.coot_validate(ctypes.byref(e)) == 2
 
 
 def test_integer_scalar_must_be_integral_R4():

@@ -68,6 +68,24 @@ def test_integer_expressions_reject_fractional_scalars_R4():
     assert coot.lower(7 * X).scalars == [7]
 
 
+def test_views_lower_to_strided_operands():
+    A = coot.Mat(torch.zeros(7 * 5, dtype=torch.float32), 7, 5)
+    base = A.data.data_ptr()
+    d = A.diag()
+    assert (d.n_rows, d.n_cols) == (5, 1)
+    lw = coot.lower(d + 100)
+    assert lw.program == P("L0 S0 ADD")
+    assert lw.operands[0] == (base, 5, 1, 5, 8)  # inc = ld + 1
+    assert coot.lower(A.diag(2) * 1).operands[0] == (base + 2 * 7 * 4, 5 - 2, 1, 3, 8)
+    assert coot.lower(A.diag(-3) * 1).operands[0] == (base + 3 * 4, 4, 1, 4, 8)
+    s = A.submat(1, 2, 4, 3)  # rows 1..4, cols 2..3
+    assert coot.lower(s * 2).operands[0] == (base + (1 + 2 * 7) * 4, 4, 2, 7, 1)
+    r = A.row(6)
+    assert coot.lower(r + r).operands == [(base + 6 * 4, 1, 5, 7, 1)]  # one operand, loaded twice
+    with pytest.raises(coot.CootError):
+        A.submat(0, 0, 7, 1)  # out of bounds
+
+
 def test_mat_layout_is_column_major():
     t = torch.arange(6, dtype=torch.float64).reshape(2, 3)  # [[0,1,2],[3,4,5]]
     m = coot.Mat.from_torch(t)

@@ -1,0 +1,142 @@
+"""Strided views (PAPER.md P:177 `Z.diag() += 100`
+diagonal / submatrix views): views as operands, as assignment targets and
+under every reduction, against the oracle on the gathered view elements."""
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from gpu_util import TORCH, requires_gpu, to_dev, to_host
+from progs import ALL, FLOATS, P, assert_elementwise, assert_reduction
+
+pytestmark = [pytest.mark.gpu, requires_gpu]
+GOLD = os.path.join(os.path.dirname(__file__), "golden", "spec_diag.txt")
+
+
+@pytest.fixture(scope="module")
+def coot():
+    import paper_2508_11385_b200 as c
+    return c
+
+
+@pytest.fixture(scope="module")
+def ctx(coot):
+    return coot.default_ctx(0)
+
+
+def dev_mat(coot, etype, m, n, stream):
+    host = oracle.fill(etype, "randu", m * n, stream=stream)
+    if etype in FLOATS:
+        host = host + oracle.DTYPES[etype](0.5)
+    return coot.Mat(to_dev(host, etype), m, n), host.reshape(n, m).T.copy()  # host (m x n)
+
+
+def test_spec_diag_example(coot, ctx):
+    g = {}
+    for line in open(GOLD):
+        if line.strip() and not line.startswith("#"):
+            k, *v = line.split()
+            g[k] = [float(x) for x in v]
+    Z = coot.Mat(torch.tensor(g["before"], dtype=torch.float64, device="cuda"), 2, 2)
+    d = Z.diag()
+    d += 100  # Z.diag() += 100
+    torch.cuda.synchronize()
+    assert Z.data.cpu().tolist() == g["after"]
+
+
+@pytest.mark.parametrize("etype", ALL)
+@pytest.mark.parametrize("k", [0, 3, -5])
+def test_diag_in_place_update(coot, ctx, etype, k):
+    m, n = 37, 29
+    Z, H = dev_mat(coot, etype, m, n, 0)
+    d = Z.diag(k)
+    idx = np.arange(len(np.diagonal(H, k)))
+    rows = idx + max(0, -k)
+    cols = idx + max(0, k)
+    diag = H[rows, cols].copy()
+    before = ctx.stats()["launches"]
+    d += 100
+    assert ctx.stats()["launches"] == before + 1 and ctx.stats()["last_path"] == -4
+    torch.cuda.synchronize()
+    want = H.copy()
+    want[rows, cols] = oracle.eval_program(etype, P("L0 S0 ADD"), [diag], [100])
+    got = to_host(Z.data, etype).reshape(n, m).T
+    assert np.array_equal(got, want)  # untouched elements unchanged, diagonal exact
+
+
+@pytest.mark.parametrize("etype", ALL)
+def test_submatrix_expression_into_dense_and_into_view(coot, ctx, etype):
+    m, n = 300, 200
+    A, HA = dev_mat(coot, etype, m, n, 1)
+    B, HB = dev_mat(coot, etype, m, n, 2)
+    a = A.submat(10, 20, 109, 139)  # 100 x 120
+    b = B.submat(50, 5, 149, 124)
+    sa = HA[10:110, 20:140].T.reshape(-1)  # column-major gather
+    sb = HB[50:150, 5:125].T.reshape(-1)
+    prog = P("S0 L0 MUL L1 ADD")
+    want = oracle.eval_program(etype, prog, [sa, sb], [3])
+    Z = (3 * a + b).eval(ctx)  # dense destination
+    torch.cuda.synchronize()
+    assert_elementwise(to_host(Z.data, etype), want, etype, max_ulp=0)
+    # the same expression written INTO another submatrix view of B (disjoint span)
+    c = B.submat(160, 130, 259, 249)
+    c.assign(3 * a + b.parent.submat(50, 5, 149, 124))
+    torch.cuda.synchronize()
+    got = to_host(B.data, etype).reshape(n, m).T
+    assert np.array_equal(got[160:260, 130:250].T.reshape(-1), want)
+    assert np.array_equal(got[:160, :], HB[:160, :])
+
+
+@pytest.mark.parametrize("etype", ALL)
+@pytest.mark.parametrize("kind", ["ACCU", "MINMAX", "NORM2"])
+def test_reductions_over_views(coot, ctx, etype, kind):
+    if kind == "NORM2" and etype not in FLOATS:
+        pytest.skip("NORM2 is float-only")
+    m, n = 500, 300
+    A, HA = dev_mat(coot, etype, m, n, 3)
+    views = {"sub": (A.submat(7, 9, 406, 258), HA[7:407, 9:259]),
+             "diag": (A.diag(), np.diagonal(HA).reshape(-1, 1)),
+             "row": (A.row(123), HA[123:124, :])}
+    for name, (v, h) in views.items():
+        flat = np.ascontiguousarray(h.T.reshape(-1))
+        want = oracle.reduce(etype, kind, flat)
+        got = {"ACCU": coot.accu, "MINMAX": coot.minmax, "NORM2": coot.norm2}[kind](v, ctx)
+        torch.cuda.synchronize()
+        g = to_host(got, etype)
+        g = g[:2] if kind == "MINMAX" else g[0]
+        assert_reduction(g, want, etype, kind, float(np.abs(flat.astype(np.float64)).sum()))
+
+
+@pytest.mark.parametrize("etype", ALL)
+@pytest.mark.parametrize("dim", [0, 1])
+def test_sum_dim_over_views(coot, ctx, etype, dim):
+    m, n = 400, 300
+    A, HA = dev_mat(coot, etype, m, n, 4)
+    v = A.submat(11, 13, 310, 212)
+    h = HA[11:311, 13:213]
+    r = coot.sum(v, dim, ctx)
+    torch.cuda.synchronize()
+    got = to_host(r.data, etype)
+    want = oracle.sum_dim(etype, dim, np.ascontiguousarray(h.T.reshape(-1)), 300, 200)
+    for i in range(got.size):
+        assert_reduction(got[i], want[i], etype, "ACCU", 1.0)
+
+
+def test_view_alias_rules(coot, ctx):
+    m, n = 64, 64
+    A, _ = dev_mat(coot, "f32", m, n, 5)
+    # destination overlapping (not identical to) an operand view -> contract error
+    with pytest.raises(coot.CootError) as ei:
+        A.submat(1, 1, 10, 10).assign(A.submat(0, 0, 9, 9) + 1)
+    assert ei.value.status == "CONTRACT"
+    # a self-overlapping destination view -> contract error
+    from paper_2508_11385_b200.api import View
+    bad = View(A, 0, 8, 8, ld=4, inc=1)
+    with pytest.raises(coot.CootError) as ei:
+        bad.assign(A.submat(20, 20, 27, 27) * 2)
+    assert ei.value.status == "CONTRACT"
+    # identical view in place is fine
+    s = A.submat(3, 3, 40, 50)
+    s *= 2
