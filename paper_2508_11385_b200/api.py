@@ -14,6 +14,7 @@ step is computed by libcoot's CUDA kernels.
 """
 from __future__ import annotations
 
+import builtins
 import ctypes
 import numbers
 
@@ -281,10 +282,11 @@ class Mat(Expr):
     def diag(self, k: int = 0) -> "View":
         """k-th diagonal as an n x 1 Col view (k > 0 above, k < 0 below the main)."""
         m, n = self.n_rows, self.n_cols
+        # (this module defines coot's own min/max; use the builtins here)
         if k >= 0:
-            length, off = max(0, min(m, n - k)), k * m
+            length, off = builtins.max(0, builtins.min(m, n - k)), k * m
         else:
-            length, off = max(0, min(m + k, n)), -k
+            length, off = builtins.max(0, builtins.min(m + k, n)), -k
         if length == 0:
             raise CootError(3, f"bounds: diagonal {k} of a {m}x{n} matrix is empty")
         return View(self, off, length, 1, ld=length, inc=m + 1)
