@@ -68,7 +68,7 @@ def test_diag_in_place_update(coot, ctx, etype, k):
 
 @pytest.mark.parametrize("etype", ALL)
 def test_submatrix_expression_into_dense_and_into_view(coot, ctx, etype):
-    m, n = 300, 200
+    m, n = 300, 300
     A, HA = dev_mat(coot, etype, m, n, 1)
     B, HB = dev_mat(coot, etype, m, n, 2)
     a = A.submat(10, 20, 109, 139)  # 100 x 120
@@ -81,11 +81,11 @@ def test_submatrix_expression_into_dense_and_into_view(coot, ctx, etype):
     torch.cuda.synchronize()
     assert_elementwise(to_host(Z.data, etype), want, etype, max_ulp=0)
     # the same expression written INTO another submatrix view of B (disjoint span)
-    c = B.submat(160, 130, 259, 249)
+    c = B.submat(160, 150, 259, 269)
     c.assign(3 * a + b.parent.submat(50, 5, 149, 124))
     torch.cuda.synchronize()
     got = to_host(B.data, etype).reshape(n, m).T
-    assert np.array_equal(got[160:260, 130:250].T.reshape(-1), want)
+    assert np.array_equal(got[160:260, 150:270].T.reshape(-1), want)
     assert np.array_equal(got[:160, :], HB[:160, :])
 
 
