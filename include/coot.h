@@ -137,11 +137,20 @@ typedef struct {
  * ACCU of floats accumulates in f64 and rounds once to eT (R10); integer
  * ACCU is modular.  NORM2 = sqrt(sum v^2), floats only (R12).
  * MIN/MAX/MINMAX of an empty expression -> COOT_ERR_CONTRACT; ACCU, NORM2 of
- * empty -> 0; SUM_DIM over a zero-length dimension -> zeros. */
+ * empty -> 0; SUM_DIM over a zero-length dimension -> zeros.
+ * Statistics ("mean, variance"; Armadillo semantics, R22), f32/f64 only:
+ *   MEAN -> 1 eT = sum / n (empty -> COOT_ERR_CONTRACT);
+ *   VAR  -> 1 eT = sum (v - mean)^2 / (n - 1)  (n == 1 -> 0; empty -> contract);
+ *   STDDEV -> 1 eT = sqrt(VAR).  One pass: shifted sums per thread merged with
+ *   Chan's pairwise update in a fixed order (deterministic).
+ * INDEX_MIN / INDEX_MAX -> 1 u64: the index (column-major linear) of the FIRST
+ *   occurrence of the smallest / largest element (empty -> contract). */
 typedef enum {
   COOT_RED_ACCU = 0, COOT_RED_MIN = 1, COOT_RED_MAX = 2, COOT_RED_MINMAX = 3,
   COOT_RED_NORM2 = 4, COOT_RED_SUM_DIM0 = 5, COOT_RED_SUM_DIM1 = 6,
-  COOT_RED_COUNT_ = 7
+  COOT_RED_MEAN = 7, COOT_RED_VAR = 8, COOT_RED_STDDEV = 9,
+  COOT_RED_INDEX_MIN = 10, COOT_RED_INDEX_MAX = 11,
+  COOT_RED_COUNT_ = 12
 } coot_reduce_kind;
 
 typedef struct coot_ctx coot_ctx;

@@ -55,6 +55,8 @@ def lib():
         L.orc_acc_final.argtypes = [vp, vp]
         L.orc_reduce.restype = i32
         L.orc_reduce.argtypes = [i32, i32, u64, vp, vp]
+        L.orc_stats.restype = i32
+        L.orc_stats.argtypes = [i32, i32, u64, vp, vp]
         L.orc_sum_dim.restype = i32
         L.orc_sum_dim.argtypes = [i32, i32, u64, u64, vp, vp]
         L.orc_run_chunked.restype = i32
@@ -126,6 +128,21 @@ def reduce(etype: str, kind: str, v: np.ndarray):
     out = np.zeros(2, dtype=dt)
     _check(lib().orc_reduce(TYPES[etype], KINDS[kind], v.size, _ptr(v), _ptr(out)), "reduce")
     return out.copy() if kind == "MINMAX" else out[0]
+
+
+STATS = {"MEAN": 0, "VAR": 1, "STDDEV": 2, "INDEX_MIN": 3, "INDEX_MAX": 4}
+
+
+def stats(etype: str, kind: str, v: np.ndarray):
+    """MEAN / VAR / STDDEV (floats; eT result) or INDEX_MIN / INDEX_MAX (int)."""
+    dt = DTYPES[etype]
+    v = np.ascontiguousarray(v, dtype=dt)
+    if kind.startswith("INDEX"):
+        out = np.zeros(1, dtype=np.uint64)
+    else:
+        out = np.zeros(1, dtype=dt)
+    _check(lib().orc_stats(TYPES[etype], STATS[kind], v.size, _ptr(v), _ptr(out)), "stats")
+    return int(out[0]) if kind.startswith("INDEX") else out[0]
 
 
 class Accumulator:

@@ -474,6 +474,74 @@ int orc_reduce(int type, int kind, uint64_t n, const void* v, void* result) {
   return orc_acc_final(&a, result);
 }
 
+/* ---- statistics ("mean, variance"; reading R22) --------------------
+ * Floats only.  mean = (sum v) / n ; var = sum (v - mean)^2 / (n - 1) with
+ * n == 1 -> 0 (Armadillo's default normalisation); stddev = sqrt(var); each
+ * rounded once to eT.  The textbook two-pass definition: pass 1 the exact-ish
+ * mean (Neumaier in long double, divided in __float128), pass 2 the Neumaier
+ * sum of squared deviations from that mean in long double.
+ * index_min / index_max: linear scan, strict comparison, so the FIRST index
+ * of the extreme value is returned (as uint64). */
+enum { ORC_MEAN = 0, ORC_VAR = 1, ORC_STDDEV = 2, ORC_IMIN = 3, ORC_IMAX = 4 };
+
+int orc_stats(int type, int kind, uint64_t n, const void* v, void* result) {
+  if (esize(type) == 0) return ORC_E_TYPE;
+  if (kind == ORC_IMIN || kind == ORC_IMAX) {
+    if (n == 0) return ORC_E_EMPTY;
+    uint64_t best = 0;
+    for (uint64_t i = 1; i < n; ++i) {
+      int better;
+      switch (type) {
+        case ORC_F32: {
+          float a = ((const float*)v)[i], b = ((const float*)v)[best];
+          better = kind == ORC_IMIN ? (a < b) : (a > b);
+          break;
+        }
+        case ORC_F64: {
+          double a = ((const double*)v)[i], b = ((const double*)v)[best];
+          better = kind == ORC_IMIN ? (a < b) : (a > b);
+          break;
+        }
+        case ORC_U32: {
+          uint32_t a = ((const uint32_t*)v)[i], b = ((const uint32_t*)v)[best];
+          better = kind == ORC_IMIN ? (a < b) : (a > b);
+          break;
+        }
+        default: {
+          int64_t a = ((const int64_t*)v)[i], b = ((const int64_t*)v)[best];
+          better = kind == ORC_IMIN ? (a < b) : (a > b);
+          break;
+        }
+      }
+      if (better) best = i;
+    }
+    *(uint64_t*)result = best;
+    return ORC_E_OK;
+  }
+  if (type != ORC_F32 && type != ORC_F64) return ORC_E_KIND;
+  if (kind < ORC_MEAN || kind > ORC_STDDEV) return ORC_E_KIND;
+  if (n == 0) return ORC_E_EMPTY;
+  long double s = 0, c = 0;
+  for (uint64_t i = 0; i < n; ++i) neumaier(&s, &c, elem_as_ld(type, v, i));
+  const __float128 mean_q = ((__float128)s + (__float128)c) / (__float128)n;
+  __float128 r;
+  if (kind == ORC_MEAN) {
+    r = mean_q;
+  } else {
+    const long double mean = (long double)mean_q;
+    long double s2 = 0, c2 = 0;
+    for (uint64_t i = 0; i < n; ++i) {
+      const long double d = elem_as_ld(type, v, i) - mean;
+      neumaier(&s2, &c2, d * d);
+    }
+    r = n > 1 ? ((__float128)s2 + (__float128)c2) / (__float128)(n - 1) : (__float128)0;
+    if (kind == ORC_STDDEV) r = sqrtq(r);
+  }
+  if (type == ORC_F32) *(float*)result = (float)r;
+  else *(double*)result = (double)r;
+  return ORC_E_OK;
+}
+
 /* ---- dimension sums (reading R3) ----------------------------------------
  * X is column-major m x n (element (i,j) at X[i + j*m]).
  * dim 0: out[j] = sum_{i=0..m-1} X(i,j)   (n_cols results, a Row)
