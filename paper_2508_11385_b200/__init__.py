@@ -8,10 +8,11 @@ native library is missing — there is no CPU fallback.
 """
 from . import _native  # noqa: F401  (raises ImportError if libcoot.so is missing)
 from ._native import CootError
-from .api import (Col, Context, Expr, Mat, Row, abs, accu, default_ctx, dot, exp, init, log,
-                  lower, max, min, minmax, norm2, partial_bytes, shard_range, sqrt, square, sum,
-                  validate)
+from .api import (Col, Context, Expr, Mat, Row, View, abs, accu, default_ctx, dot, exp,
+                  index_max, index_min, init, log, lower, max, mean, min, minmax, norm2,
+                  partial_bytes, shard_range, sqrt, square, stddev, sum, validate, var)
 
-__all__ = ["Col", "Context", "CootError", "Expr", "Mat", "Row", "abs", "accu", "default_ctx",
-           "dot", "exp", "init", "log", "lower", "max", "min", "minmax", "norm2",
-           "partial_bytes", "shard_range", "sqrt", "square", "sum", "validate"]
+__all__ = ["Col", "Context", "CootError", "Expr", "Mat", "Row", "View", "abs", "accu",
+           "default_ctx", "dot", "exp", "index_max", "index_min", "init", "log", "lower", "max",
+           "mean", "min", "minmax", "norm2", "partial_bytes", "shard_range", "sqrt", "square",
+           "stddev", "sum", "validate", "var"]

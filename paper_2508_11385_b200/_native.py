@@ -23,7 +23,8 @@ PARTIAL_BYTES = 32
 ELEM = {"f32": 0, "f64": 1, "u32": 2, "s64": 3}
 OP = {"LOAD": 0, "SCALAR": 1, "NEG": 2, "ABS": 3, "SQUARE": 4, "SQRT": 5, "EXP": 6, "LOG": 7,
       "ADD": 8, "SUB": 9, "MUL": 10, "DIV": 11, "MIN": 12, "MAX": 13}
-KIND = {"ACCU": 0, "MIN": 1, "MAX": 2, "MINMAX": 3, "NORM2": 4, "SUM_DIM0": 5, "SUM_DIM1": 6}
+KIND = {"ACCU": 0, "MIN": 1, "MAX": 2, "MINMAX": 3, "NORM2": 4, "SUM_DIM0": 5, "SUM_DIM1": 6,
+        "MEAN": 7, "VAR": 8, "STDDEV": 9, "INDEX_MIN": 10, "INDEX_MAX": 11}
 FILL = {"randu": 0, "ones": 1, "iota": 2, "modk": 3, "colidx": 4, "rowidx": 5, "zeros": 6}
 STATUS = {0: "OK", 1: "CONFIG", 2: "CONFORM", 3: "BOUNDS", 4: "RESOURCE", 5: "CONTRACT", 6: "DEVICE"}
 INIT_PRINT_INFO = 1

@@ -496,7 +496,8 @@ def _reduce(e, kind, ctx=None, out: Mat | None = None):
     lw = lower(as_expr(e))
     ctx = ctx or default_ctx(lw.device_index())
     shape = {"MINMAX": (2,), "SUM_DIM0": (lw.n_cols,), "SUM_DIM1": (lw.n_rows,)}.get(kind, (1,))
-    result = torch.empty(shape, dtype=TORCH_DTYPE[lw.elem], device=lw.device())
+    dtype = torch.int64 if kind.startswith("INDEX") else TORCH_DTYPE[lw.elem]
+    result = torch.empty(shape, dtype=dtype, device=lw.device())
     ctx.reduce(lw.elem, lw.n_rows, lw.n_cols, lw.program, lw.operands, lw.scalars, kind, result,
                out.data if out is not None else None)
     return result
@@ -543,3 +544,27 @@ def max(a, b=None, ctx=None):  # noqa: A001
 
 def minmax(e, ctx=None):
     return _reduce(e, "MINMAX", ctx)
+
+
+# ---- statistics ("mean, variance"; Armadillo semantics, R22) ----------
+def mean(e, ctx=None):
+    """Mean of all elements (floats), one launch."""
+    return _reduce(e, "MEAN", ctx)
+
+
+def var(e, ctx=None):
+    """Variance with n-1 normalisation (Armadillo default), one pass, one launch."""
+    return _reduce(e, "VAR", ctx)
+
+
+def stddev(e, ctx=None):
+    return _reduce(e, "STDDEV", ctx)
+
+
+def index_min(e, ctx=None):
+    """Column-major linear index of the first smallest element (int64 tensor)."""
+    return _reduce(e, "INDEX_MIN", ctx)
+
+
+def index_max(e, ctx=None):
+    return _reduce(e, "INDEX_MAX", ctx)

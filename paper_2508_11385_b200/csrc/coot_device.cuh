@@ -23,7 +23,10 @@ namespace coot {
 typedef long long s64;
 typedef unsigned long long u64;
 
-enum AccKind { ACC_NONE = 0, ACC_SUM = 1, ACC_SUMSQ = 2, ACC_MINMAX = 3 };
+enum AccKind {
+  ACC_NONE = 0, ACC_SUM = 1, ACC_SUMSQ = 2, ACC_MINMAX = 3,
+  ACC_VAR = 4, ACC_IMIN = 5, ACC_IMAX = 6
+};
 enum FinalMode { FINAL_ROUND = 0, FINAL_PARTIAL = 1 };
 
 constexpr int kThreads = 256;
@@ -409,19 +412,62 @@ __device__ __forceinline__ typename SumT<T>::type unit_sum(const T (&v)[W]) {
   }
 }
 
+// Per-thread / per-block / per-rank accumulator for every reduction kind.
+//  ACC_SUM, ACC_SUMSQ: s (f64 for floats, u64 modular for ints)
+//  ACC_MINMAX:         mn, mx
+//  ACC_VAR:            n elements, shift c, s1 = sum(x - c), s2 = sum(x - c)^2 in
+//                      f64 (c = the thread's first element, so the shifted sums
+//                      do not cancel); merged with Chan et al.'s pairwise update,
+//                      after which c is the mean, s1 = 0 and s2 = M2
+//  ACC_IMIN, ACC_IMAX: best value + its (first) global index
 template <class T, int ACC>
 struct Accum {
   typedef typename SumT<T>::type S;
   S s;
   T mn, mx;
+  u64 n, idx;
+  double c, s1, s2;
   __device__ __forceinline__ void init() {
     s = S(0);
     mn = MinMaxId<T>::lo();
     mx = MinMaxId<T>::hi();
+    n = 0;
+    idx = ~0ull;
+    c = s1 = s2 = 0.0;
+  }
+  // Accumulate W consecutive elements whose first element has global index
+  // `base` (only the index-returning kinds use it).
+  template <int W>
+  __device__ __forceinline__ void add_at(const T (&v)[W], u64 base) {
+    if constexpr (ACC == ACC_IMIN || ACC == ACC_IMAX) {
+#pragma unroll
+      for (int w = 0; w < W; ++w) {
+        // strict comparison: within a thread indices increase, so the first
+        // occurrence wins; the sentinel idx admits the very first element
+        const bool better = (ACC == ACC_IMIN) ? (v[w] < mn) : (mx < v[w]);
+        if (idx == ~0ull || better) {
+          if constexpr (ACC == ACC_IMIN) mn = v[w];
+          else mx = v[w];
+          idx = base + w;
+        }
+      }
+    } else {
+      add<W>(v);
+    }
   }
   template <int W>
   __device__ __forceinline__ void add(const T (&v)[W]) {
-    if constexpr (ACC == ACC_SUM) {
+    if constexpr (ACC == ACC_VAR) {
+#pragma unroll
+      for (int w = 0; w < W; ++w) {
+        const double x = (double)v[w];
+        if (n == 0) c = x;
+        const double d = __dsub_rn(x, c);
+        s1 = __dadd_rn(s1, d);
+        s2 = __fma_rn(d, d, s2);
+        ++n;
+      }
+    } else if constexpr (ACC == ACC_SUM) {
       s = sum_add<S>(s, unit_sum<T, W>(v));
     } else if constexpr (ACC == ACC_SUMSQ) {
       T q[W];
@@ -436,7 +482,7 @@ struct Accum {
       }
     }
   }
-  // Fixed xor-butterfly: every lane ends with the same value.
+  // Fixed xor-butterfly (a deterministic tree per lane).
   __device__ __forceinline__ void warp_reduce() {
 #pragma unroll
     for (int m = 16; m >= 1; m >>= 1) {
@@ -445,6 +491,16 @@ struct Accum {
       } else if constexpr (ACC == ACC_MINMAX) {
         mn = bin<COOT_OP_MIN>(mn, shfl_xor(mn, m));
         mx = bin<COOT_OP_MAX>(mx, shfl_xor(mx, m));
+      } else if constexpr (ACC != ACC_NONE) {
+        Accum o = *this;
+        o.n = shfl_xor((u64)n, m);
+        o.idx = shfl_xor((u64)idx, m);
+        o.c = shfl_xor(c, m);
+        o.s1 = shfl_xor(s1, m);
+        o.s2 = shfl_xor(s2, m);
+        o.mn = shfl_xor(mn, m);
+        o.mx = shfl_xor(mx, m);
+        merge(o);
       }
     }
   }
@@ -454,13 +510,52 @@ struct Accum {
     } else if constexpr (ACC == ACC_MINMAX) {
       mn = bin<COOT_OP_MIN>(mn, o.mn);
       mx = bin<COOT_OP_MAX>(mx, o.mx);
+    } else if constexpr (ACC == ACC_VAR) {
+      if (o.n == 0) return;
+      if (n == 0) {
+        *this = o;
+        return;
+      }
+      // (n, mean, M2) of both sides, then Chan's pairwise combination
+      const double na = (double)n, nb = (double)o.n, nab = (double)(n + o.n);
+      const double ma = __dadd_rn(c, __ddiv_rn(s1, na));
+      const double mb = __dadd_rn(o.c, __ddiv_rn(o.s1, nb));
+      const double m2a = __dsub_rn(s2, __ddiv_rn(__dmul_rn(s1, s1), na));
+      const double m2b = __dsub_rn(o.s2, __ddiv_rn(__dmul_rn(o.s1, o.s1), nb));
+      const double delta = __dsub_rn(mb, ma);
+      c = __dadd_rn(ma, __ddiv_rn(__dmul_rn(delta, nb), nab));
+      s2 = __dadd_rn(__dadd_rn(m2a, m2b),
+                     __ddiv_rn(__dmul_rn(__dmul_rn(delta, delta), __dmul_rn(na, nb)), nab));
+      s1 = 0.0;
+      n += o.n;
+    } else if constexpr (ACC == ACC_IMIN || ACC == ACC_IMAX) {
+      if (o.idx == ~0ull) return;
+      const T ov = ACC == ACC_IMIN ? o.mn : o.mx, v = ACC == ACC_IMIN ? mn : mx;
+      const bool better = ACC == ACC_IMIN ? (ov < v) : (v < ov);
+      if (idx == ~0ull || better || (!(v < ov) && !(ov < v) && o.idx < idx)) {
+        mn = o.mn;
+        mx = o.mx;
+        idx = o.idx;
+      }
     }
   }
   __device__ __forceinline__ Rec to_rec(u64 count) const {
     Rec r;
+    r.count = count;
+    r.pad = 0;
     if constexpr (ACC == ACC_MINMAX) {
       r.a = to_bits<T>(mn);
       r.b = to_bits<T>(mx);
+    } else if constexpr (ACC == ACC_VAR) {
+      // (mean, M2, n): the merged form of the shifted sums
+      const double mean = n ? __dadd_rn(c, __ddiv_rn(s1, (double)n)) : 0.0;
+      const double m2 = n ? __dsub_rn(s2, __ddiv_rn(__dmul_rn(s1, s1), (double)n)) : 0.0;
+      r.a = (u64)__double_as_longlong(mean);
+      r.b = (u64)__double_as_longlong(m2);
+      r.count = n;
+    } else if constexpr (ACC == ACC_IMIN || ACC == ACC_IMAX) {
+      r.a = to_bits<T>(ACC == ACC_IMIN ? mn : mx);
+      r.b = idx;
     } else if constexpr (is_float<T>()) {
       r.a = (u64)__double_as_longlong((double)s);
       r.b = 0;
@@ -468,8 +563,6 @@ struct Accum {
       r.a = (u64)s;
       r.b = 0;
     }
-    r.count = count;
-    r.pad = 0;
     return r;
   }
   __device__ __forceinline__ void from_rec(const Rec& r) {
@@ -478,6 +571,14 @@ struct Accum {
       // empty producers publish the identities (+inf/-inf, UINT_MAX/0, ...)
       mn = scalar_as<T>(r.a);
       mx = scalar_as<T>(r.b);
+    } else if constexpr (ACC == ACC_VAR) {
+      c = __longlong_as_double((long long)r.a);
+      s2 = __longlong_as_double((long long)r.b);
+      s1 = 0.0;
+      n = r.count;
+    } else if constexpr (ACC == ACC_IMIN || ACC == ACC_IMAX) {
+      mn = mx = scalar_as<T>(r.a);
+      idx = r.b;
     } else if constexpr (is_float<T>()) {
       s = __longlong_as_double((long long)r.a);
     } else {
@@ -496,11 +597,31 @@ __device__ __forceinline__ Rec load_rec_cg(const Rec* p) {
   return r;
 }
 
-// Round the combined accumulator into the user-visible result (eT).
+template <class T>
+__device__ __forceinline__ T round_to(double x) {
+  if constexpr (sizeof(T) == 4 && is_float<T>()) return __double2float_rn(x);
+  else return (T)x;
+}
+
+// Round the combined accumulator into the user-visible result (eT, or a u64
+// index).  `count` = number of elements reduced (MEAN's divisor).
 template <class T, int ACC>
-__device__ __forceinline__ void write_final(const Accum<T, ACC>& acc, uint32_t kind, void* result) {
+__device__ __forceinline__ void write_final(const Accum<T, ACC>& acc, uint32_t kind, void* result,
+                                            u64 count) {
   T* out = reinterpret_cast<T*>(result);
-  if constexpr (ACC == ACC_MINMAX) {
+  if constexpr (ACC == ACC_VAR) {
+    const double var = acc.n > 1 ? __ddiv_rn(acc.s2 - __ddiv_rn(__dmul_rn(acc.s1, acc.s1),
+                                                                (double)acc.n),
+                                             (double)(acc.n - 1))
+                                 : 0.0;
+    const double v = var > 0.0 ? var : 0.0;
+    out[0] = round_to<T>(kind == COOT_RED_STDDEV ? __dsqrt_rn(v) : v);
+  } else if constexpr (ACC == ACC_IMIN || ACC == ACC_IMAX) {
+    *reinterpret_cast<u64*>(result) = acc.idx;
+  } else if constexpr (ACC == ACC_SUM && is_float<T>()) {
+    if (kind == COOT_RED_MEAN) out[0] = round_to<T>(__ddiv_rn(acc.s, (double)count));
+    else out[0] = round_to<T>(acc.s);
+  } else if constexpr (ACC == ACC_MINMAX) {
     if (kind == COOT_RED_MIN) out[0] = acc.mn;
     else if (kind == COOT_RED_MAX) out[0] = acc.mx;
     else {
@@ -571,7 +692,7 @@ __device__ __forceinline__ void grid_finish(const Accum<T, ACC>& block_total, Re
       if (final_mode == FINAL_PARTIAL) {
         *reinterpret_cast<Rec*>(result) = acc.to_rec(count);
       } else {
-        write_final<T, ACC>(acc, kind, result);
+        write_final<T, ACC>(acc, kind, result, count);
       }
       *ticket = 0u;
     }

@@ -269,7 +269,7 @@ __global__ void __launch_bounds__(kThreads, EV::kInterp ? 1 : COOT_CAT_MINB)
     load_elem<T, EV>(a, e, in);
     EV::template eval<T, 1>(in, a, v);
     if (out) out[e] = v[0];
-    acc.template add<1>(v);
+    acc.template add_at<1>(v, e);
   }
   {
     const uint32_t nthr32 = (uint32_t)nthr, tid32 = (uint32_t)tid;
@@ -299,7 +299,7 @@ __global__ void __launch_bounds__(kThreads, EV::kInterp ? 1 : COOT_CAT_MINB)
               memcpy(&r, &v[0], 16);
               st16(po + u + j * nthr32, r);
             }
-            acc.template add<W>(v);
+            acc.template add_at<W>(v, a.head + (s0 + u + (u64)j * nthr32) * W);
           }
         }
 #pragma unroll
@@ -317,7 +317,7 @@ __global__ void __launch_bounds__(kThreads, EV::kInterp ? 1 : COOT_CAT_MINB)
     load_elem<T, EV>(a, e, in);
     EV::template eval<T, 1>(in, a, v);
     if (out) out[e] = v[0];
-    acc.template add<1>(v);
+    acc.template add_at<1>(v, e);
   }
 
   if constexpr (ACC != ACC_NONE) {
@@ -355,7 +355,7 @@ __global__ void __launch_bounds__(kThreads) fused_strided_kernel(const __grid_co
     }
     EV::template eval<T, 1>(in, a, v);
     if (out) out[i * a.out_inc + j * a.out_ld] = v[0];
-    acc.template add<1>(v);
+    acc.template add_at<1>(v, e);
     i += di;
     j += dj;
     if (i >= m) {
@@ -459,7 +459,7 @@ __global__ void __launch_bounds__(kTmaThreads, tma_min_ctas<EV>())
       load_elem<T, EV>(a, e, in);
       EV::template eval<T, 1>(in, a, v);
       if (out) out[e] = v[0];
-      acc.template add<1>(v);
+      acc.template add_at<1>(v, e);
     }
     uint4* po = out ? reinterpret_cast<uint4*>(reinterpret_cast<char*>(out) + boff) : nullptr;
     uint32_t s = 0, ph = 0;
@@ -486,7 +486,7 @@ __global__ void __launch_bounds__(kTmaThreads, tma_min_ctas<EV>())
               memcpy(&r, &vj[0], 16);
               st16(po + u0 + ij, r);
             }
-            acc.template add<W>(vj);
+            acc.template add_at<W>(vj, a.head + (u0 + ij) * W);
           }
         }
       }
@@ -502,7 +502,7 @@ __global__ void __launch_bounds__(kTmaThreads, tma_min_ctas<EV>())
       load_elem<T, EV>(a, e, in);
       EV::template eval<T, 1>(in, a, v);
       if (out) out[e] = v[0];
-      acc.template add<1>(v);
+      acc.template add_at<1>(v, e);
     }
   }
 

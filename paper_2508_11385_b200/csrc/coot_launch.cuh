@@ -38,19 +38,26 @@ FusedFn catalog_kernel(int driver) {
   }
 }
 
+// The statistics / index reductions (ACC_VAR, ACC_IMIN, ACC_IMAX) are
+// instantiated for the plain-matrix program [L0] and the interpreter only (the
+// host routes other catalog shapes to the interpreter for them).
 template <class T, int ACC>
 FusedFn pick_fused_acc(int catalog, int interp_large, int driver) {
-  if constexpr (ACC == ACC_SUMSQ && !is_float<T>()) {
+  if constexpr ((ACC == ACC_SUMSQ || ACC == ACC_VAR) && !is_float<T>()) {
     return nullptr;
   } else {
-    switch (catalog) {
+    if constexpr (ACC >= ACC_VAR) {
+      if (catalog == 0) return catalog_kernel<T, ACC, CL(0)>(driver);
+    } else {
+      switch (catalog) {
 #define COOT_X(id, ...) \
   case id:              \
     return catalog_kernel<T, ACC, __VA_ARGS__>(driver);
-      COOT_CATALOG(COOT_X)
+        COOT_CATALOG(COOT_X)
 #undef COOT_X
-      default:
-        break;
+        default:
+          break;
+      }
     }
     if (interp_large) return driver_kernel<T, ACC, InterpEval<8, 8>, 1>(driver);
     return driver_kernel<T, ACC, InterpEval<4, 4>, 1>(driver);
@@ -64,6 +71,9 @@ FusedFn pick_fused(const FusedPlan& p) {
     case ACC_SUM: return pick_fused_acc<T, ACC_SUM>(p.catalog, p.interp_large, p.driver);
     case ACC_SUMSQ: return pick_fused_acc<T, ACC_SUMSQ>(p.catalog, p.interp_large, p.driver);
     case ACC_MINMAX: return pick_fused_acc<T, ACC_MINMAX>(p.catalog, p.interp_large, p.driver);
+    case ACC_VAR: return pick_fused_acc<T, ACC_VAR>(p.catalog, p.interp_large, p.driver);
+    case ACC_IMIN: return pick_fused_acc<T, ACC_IMIN>(p.catalog, p.interp_large, p.driver);
+    case ACC_IMAX: return pick_fused_acc<T, ACC_IMAX>(p.catalog, p.interp_large, p.driver);
   }
   return nullptr;
 }
@@ -158,12 +168,17 @@ __global__ void combine_rec_kernel(const Rec* parts, uint32_t nparts, uint32_t k
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   Accum<T, ACC> acc;
   acc.init();
+  u64 before = 0;  // elements of the parts before p: shards are contiguous blocks
   for (uint32_t p = 0; p < nparts; ++p) {
     Accum<T, ACC> o;
     o.from_rec(parts[p]);
+    if constexpr (ACC == ACC_IMIN || ACC == ACC_IMAX) {
+      if (o.idx != ~0ull) o.idx += before;  // shard-local -> global index
+    }
     acc.merge(o);
+    before += parts[p].count;
   }
-  write_final<T, ACC>(acc, kind, result);
+  write_final<T, ACC>(acc, kind, result, before);
 }
 
 // Vector partials (SUM_DIM*): result[i] = round(sum_p parts[p][i]), p in order.
@@ -210,6 +225,15 @@ cudaError_t launch_combine_t(uint32_t kind, int acc, const void* parts, uint32_t
     case ACC_MINMAX:
       combine_rec_kernel<T, ACC_MINMAX><<<1, 32, 0, s>>>(r, nparts, kind, result);
       break;
+    case ACC_VAR:
+      if constexpr (is_float<T>()) {
+        combine_rec_kernel<T, ACC_VAR><<<1, 32, 0, s>>>(r, nparts, kind, result);
+        break;
+      } else {
+        return cudaErrorInvalidValue;
+      }
+    case ACC_IMIN: combine_rec_kernel<T, ACC_IMIN><<<1, 32, 0, s>>>(r, nparts, kind, result); break;
+    case ACC_IMAX: combine_rec_kernel<T, ACC_IMAX><<<1, 32, 0, s>>>(r, nparts, kind, result); break;
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();
@@ -228,6 +252,15 @@ cudaError_t launch_empty_rec_t(int acc, void* out, cudaStream_t s) {
         return cudaErrorInvalidValue;
       }
     case ACC_MINMAX: empty_rec_kernel<T, ACC_MINMAX><<<1, 1, 0, s>>>(r); break;
+    case ACC_VAR:
+      if constexpr (is_float<T>()) {
+        empty_rec_kernel<T, ACC_VAR><<<1, 1, 0, s>>>(r);
+        break;
+      } else {
+        return cudaErrorInvalidValue;
+      }
+    case ACC_IMIN: empty_rec_kernel<T, ACC_IMIN><<<1, 1, 0, s>>>(r); break;
+    case ACC_IMAX: empty_rec_kernel<T, ACC_IMAX><<<1, 1, 0, s>>>(r); break;
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();
@@ -277,6 +310,20 @@ cudaError_t launch_fill_t(uint32_t kind, u64 seed, u64 stream, u64 start, u64 co
                                            k ? k : 1, reinterpret_cast<T*>(out));
   return cudaGetLastError();
 }
+
+// Each type's fused kernels are instantiated per reduction kind in their own
+// translation unit (kernels_<type>_acc<k>.cu) so the build parallelises; the
+// type's main unit sees them as extern templates.
+#define COOT_EXTERN_ACC(T)                                                  \
+  extern template FusedFn pick_fused_acc<T, ACC_NONE>(int, int, int);       \
+  extern template FusedFn pick_fused_acc<T, ACC_SUM>(int, int, int);        \
+  extern template FusedFn pick_fused_acc<T, ACC_SUMSQ>(int, int, int);      \
+  extern template FusedFn pick_fused_acc<T, ACC_MINMAX>(int, int, int);     \
+  extern template FusedFn pick_fused_acc<T, ACC_VAR>(int, int, int);        \
+  extern template FusedFn pick_fused_acc<T, ACC_IMIN>(int, int, int);       \
+  extern template FusedFn pick_fused_acc<T, ACC_IMAX>(int, int, int);
+
+#define COOT_INSTANTIATE_ACC(T, ACC) template FusedFn pick_fused_acc<T, ACC>(int, int, int);
 
 #define COOT_INSTANTIATE(T)                                                                     \
   template cudaError_t launch_fused_t<T>(const FusedPlan&, const FusedArgs&, cudaStream_t);   \

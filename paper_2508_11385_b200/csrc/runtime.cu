@@ -321,12 +321,29 @@ int acc_for_kind(uint32_t kind) {
     case COOT_RED_MIN:
     case COOT_RED_MAX:
     case COOT_RED_MINMAX: return coot::ACC_MINMAX;
+    case COOT_RED_MEAN: return coot::ACC_SUM;
+    case COOT_RED_VAR:
+    case COOT_RED_STDDEV: return coot::ACC_VAR;
+    case COOT_RED_INDEX_MIN: return coot::ACC_IMIN;
+    case COOT_RED_INDEX_MAX: return coot::ACC_IMAX;
   }
   return -1;
 }
 
+bool float_only_kind(uint32_t kind) {
+  return kind == COOT_RED_NORM2 || kind == COOT_RED_MEAN || kind == COOT_RED_VAR ||
+         kind == COOT_RED_STDDEV;
+}
+bool nonempty_kind(uint32_t kind) {  // undefined over zero elements
+  return kind == COOT_RED_MIN || kind == COOT_RED_MAX || kind == COOT_RED_MINMAX ||
+         kind == COOT_RED_MEAN || kind == COOT_RED_VAR || kind == COOT_RED_STDDEV ||
+         kind == COOT_RED_INDEX_MIN || kind == COOT_RED_INDEX_MAX;
+}
+
 size_t result_bytes(uint32_t kind, size_t es, u64 m, u64 n) {
   switch (kind) {
+    case COOT_RED_INDEX_MIN:
+    case COOT_RED_INDEX_MAX: return 8;
     case COOT_RED_MINMAX: return 2 * es;
     case COOT_RED_SUM_DIM0: return n * es;
     case COOT_RED_SUM_DIM1: return m * es;
@@ -506,6 +523,7 @@ coot_status run_fused(coot_ctx* ctx, const coot_expr* e, const Shape& sh, int ac
   a.kind = kind;
 
   p.catalog = (ctx->flags & COOT_INIT_FORCE_INTERP) ? -1 : match_catalog(e);
+  if (acc >= coot::ACC_VAR && p.catalog > 0) p.catalog = -1;  // see pick_fused_acc
   p.interp_large = (e->n_operands > 4 || sh.max_depth > 4) ? 1 : 0;
   p.acc = acc;
   p.grid = (unsigned)grid;
@@ -692,14 +710,13 @@ coot_status reduce_common(coot_ctx* ctx, const coot_expr* e, uint32_t kind, void
   if (!result) return fail(COOT_ERR_CONTRACT, "contract: result is NULL");
   const size_t es = elem_size(e->elem);
   const u64 n = e->n_rows * e->n_cols;
-  if (kind == COOT_RED_NORM2 && !is_float_elem(e->elem))
-    return fail(COOT_ERR_CONTRACT, "contract: NORM2 is defined for f32/f64 only");
+  if (float_only_kind(kind) && !is_float_elem(e->elem))
+    return fail(COOT_ERR_CONTRACT, "contract: reduction kind %u is defined for f32/f64 only", kind);
   const bool dim = kind == COOT_RED_SUM_DIM0 || kind == COOT_RED_SUM_DIM1;
   if (dim && out)
     return fail(COOT_ERR_CONTRACT, "contract: out_or_null must be NULL for SUM_DIM reductions");
-  if (final_mode == coot::FINAL_ROUND && n == 0 &&
-      (kind == COOT_RED_MIN || kind == COOT_RED_MAX || kind == COOT_RED_MINMAX))
-    return fail(COOT_ERR_CONTRACT, "contract: min/max of an empty expression");
+  if (final_mode == coot::FINAL_ROUND && n == 0 && nonempty_kind(kind))
+    return fail(COOT_ERR_CONTRACT, "contract: reduction kind %u of an empty expression", kind);
   if (out && reinterpret_cast<uintptr_t>(out) % es)
     return fail(COOT_ERR_CONTRACT, "contract: out is not aligned to its element size");
   const coot_operand outv = dense_view(out, e->n_rows, e->n_cols);
@@ -896,8 +913,8 @@ coot_status coot_combine(coot_ctx* ctx, uint32_t elem, uint32_t kind, const void
   if (st != COOT_OK) return st;
   if (elem_size(elem) == 0) return fail(COOT_ERR_CONTRACT, "contract: unknown element type %u", elem);
   if (kind >= COOT_RED_COUNT_) return fail(COOT_ERR_CONTRACT, "contract: unknown reduction kind %u", kind);
-  if (kind == COOT_RED_NORM2 && !is_float_elem(elem))
-    return fail(COOT_ERR_CONTRACT, "contract: NORM2 is defined for f32/f64 only");
+  if (float_only_kind(kind) && !is_float_elem(elem))
+    return fail(COOT_ERR_CONTRACT, "contract: reduction kind %u is defined for f32/f64 only", kind);
   if (nparts == 0) return fail(COOT_ERR_CONTRACT, "contract: combine of zero partials");
   if (!partials || !result) return fail(COOT_ERR_CONTRACT, "contract: NULL partials/result");
   const bool dim = kind == COOT_RED_SUM_DIM0 || kind == COOT_RED_SUM_DIM1;

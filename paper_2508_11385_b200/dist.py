@@ -72,7 +72,8 @@ class DistReducer:
             e1.record(self.ctx.stream)
             kernel_events.append((e0, e1))
         parts = allgather_partials(self._rec, self.group)
-        res = torch.empty(2, dtype=TORCH_DTYPE[lw.elem], device=self.ctx.device)
+        dtype = torch.int64 if kind.startswith("INDEX") else TORCH_DTYPE[lw.elem]
+        res = torch.empty(2, dtype=dtype, device=self.ctx.device)
         self.ctx.combine(lw.elem, kind, parts, self.world, 1, res)
         return res
 
