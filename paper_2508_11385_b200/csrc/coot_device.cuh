@@ -61,6 +61,9 @@ struct FusedArgs {
   u64 m;                // rows of the expression
   u64 ld[COOT_MAX_OPERANDS], inc[COOT_MAX_OPERANDS];
   u64 out_ld, out_inc;
+  // column-segmented view path: pieces = (column, segment of seg_len rows)
+  u64 ncols, seg_len;
+  uint32_t nseg;
   uint16_t key[COOT_MAX_INSTR];  // interpreter dispatch index: op * 9 + depth
   uint8_t arg[COOT_MAX_INSTR];
 };
@@ -440,16 +443,22 @@ struct Accum {
   template <int W>
   __device__ __forceinline__ void add_at(const T (&v)[W], u64 base) {
     if constexpr (ACC == ACC_IMIN || ACC == ACC_IMAX) {
+      // best of the unit first (strict comparisons: the first occurrence wins,
+      // indices increase within a thread), then one comparison with the
+      // running best; the sentinel idx admits the very first element
+      T bv = v[0];
+      int bw = 0;
 #pragma unroll
-      for (int w = 0; w < W; ++w) {
-        // strict comparison: within a thread indices increase, so the first
-        // occurrence wins; the sentinel idx admits the very first element
-        const bool better = (ACC == ACC_IMIN) ? (v[w] < mn) : (mx < v[w]);
-        if (idx == ~0ull || better) {
-          if constexpr (ACC == ACC_IMIN) mn = v[w];
-          else mx = v[w];
-          idx = base + w;
-        }
+      for (int w = 1; w < W; ++w) {
+        const bool better = (ACC == ACC_IMIN) ? (v[w] < bv) : (bv < v[w]);
+        bv = better ? v[w] : bv;
+        bw = better ? w : bw;
+      }
+      const bool better = (ACC == ACC_IMIN) ? (bv < mn) : (mx < bv);
+      if (idx == ~0ull || better) {
+        if constexpr (ACC == ACC_IMIN) mn = bv;
+        else mx = bv;
+        idx = base + (u64)bw;
       }
     } else {
       add<W>(v);
@@ -458,15 +467,17 @@ struct Accum {
   template <int W>
   __device__ __forceinline__ void add(const T (&v)[W]) {
     if constexpr (ACC == ACC_VAR) {
+      if (n == 0) c = (double)v[0];  // the shift: the thread's first element
+      double a1 = 0.0, a2 = 0.0;     // the unit's shifted sums, then one update each
 #pragma unroll
       for (int w = 0; w < W; ++w) {
-        const double x = (double)v[w];
-        if (n == 0) c = x;
-        const double d = __dsub_rn(x, c);
-        s1 = __dadd_rn(s1, d);
-        s2 = __fma_rn(d, d, s2);
-        ++n;
+        const double d = __dsub_rn((double)v[w], c);
+        a1 = __dadd_rn(a1, d);
+        a2 = __fma_rn(d, d, a2);
       }
+      s1 = __dadd_rn(s1, a1);
+      s2 = __dadd_rn(s2, a2);
+      n += W;
     } else if constexpr (ACC == ACC_SUM) {
       s = sum_add<S>(s, unit_sum<T, W>(v));
     } else if constexpr (ACC == ACC_SUMSQ) {

@@ -509,6 +509,138 @@ __global__ void __launch_bounds__(kTmaThreads, tma_min_ctas<EV>())
   if constexpr (ACC != ACC_NONE) {
     Accum<T, ACC> bt = block_reduce<T, ACC>(acc);
     grid_finish<T, ACC>(bt, a.partials, a.ticket, a.final_mode, a.kind, a.result, a.count);
+  } else {
+    __syncthreads();  // the producer stays resident until every staged tile is consumed
+  }
+}
+
+// ---- views with contiguous columns (submatrix / column / row-block views) ------
+// When every operand and the destination have inc == 1 and their column starts
+// share one 16-byte misalignment (ld * sizeof(T) % 16 == 0, equal base
+// misalignment), each column of the view is a contiguous run: the same
+// producer / consumer TMA ring as fused_tma_kernel streams it, piece by piece
+// (piece = (column j, segment s) of seg_len rows), with scalar head / tail
+// elements per piece.  Interpreter evaluators only (views never use the
+// catalog), element index for index reductions = j * m + i.
+template <class T, int ACC, class EV>
+__global__ void __launch_bounds__(kTmaThreads, tma_min_ctas<EV>())
+    fused_cols_tma_kernel(const __grid_constant__ FusedArgs a) {
+  constexpr int W = Unit<T>::W;
+  constexpr int K = EV::K;
+  extern __shared__ __align__(128) unsigned char smem[];
+  const uint32_t nk = a.n_operands;
+  const uint32_t S = a.stages, TU = a.tile_units;
+  const uint32_t tile_bytes = TU * 16u;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)S * nk * tile_bytes);
+  uint64_t* empty = full + S;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (uint32_t s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kConsumerWarps);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  Accum<T, ACC> acc;
+  acc.init();
+  const u64 npieces = a.ncols * a.nseg, m = a.m;
+  const uintptr_t base0 = reinterpret_cast<uintptr_t>(a.in[0]);
+  // geometry of piece p (identical on producer and consumers)
+  auto piece = [&](u64 p, u64& j, u64& r0, u64& len, u64& head, u64& nun) {
+    j = p / a.nseg;
+    r0 = (p % a.nseg) * a.seg_len;
+    len = (m - r0) < a.seg_len ? (m - r0) : a.seg_len;
+    const uintptr_t mis = (base0 + (j * a.ld[0] + r0) * sizeof(T)) & 15;
+    head = ((16 - mis) & 15) / sizeof(T);
+    if (head > len) head = len;
+    nun = (len - head) / W;
+  };
+  if (warp == kConsumerWarps) {
+    if (lane == 0) {
+      const uint64_t pol = policy_evict_first();
+      uint32_t s = 0, ph = 0;
+      u64 i = 0;
+      for (u64 p = blockIdx.x; p < npieces; p += gridDim.x) {
+        u64 j, r0, len, head, nun;
+        piece(p, j, r0, len, head, nun);
+        for (u64 u0 = 0; u0 < nun; u0 += TU, ++i) {
+          if (i >= S) mbar_wait(&empty[s], ph ^ 1u);
+          const uint32_t nu = (uint32_t)((nun - u0) < TU ? (nun - u0) : TU);
+          mbar_expect_tx(&full[s], nu * 16u * nk);
+          for (uint32_t k = 0; k < nk; ++k)
+            bulk_g2s(smem + ((size_t)s * nk + k) * tile_bytes,
+                     reinterpret_cast<const char*>(a.in[k]) +
+                         (j * a.ld[k] + r0 + head) * sizeof(T) + u0 * 16,
+                     nu * 16u, &full[s], pol);
+          if (++s == S) {
+            s = 0;
+            ph ^= 1u;
+          }
+        }
+      }
+    }
+  } else {
+    T* out = reinterpret_cast<T*>(a.out);
+    uint32_t s = 0, ph = 0;
+    constexpr int UD = units_per_dispatch<EV>();
+    for (u64 p = blockIdx.x; p < npieces; p += gridDim.x) {
+      u64 j, r0, len, head, nun;
+      piece(p, j, r0, len, head, nun);
+      const u64 e0 = j * m + r0;  // linear index of the piece's first element
+      auto scalar_elem = [&](u64 i) {
+        T in[K][1], v[1];
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+          if (k < (int)nk)
+            in[k][0] = __ldcg(reinterpret_cast<const T*>(a.in[k]) + j * a.ld[k] + r0 + i);
+          else
+            in[k][0] = T(0);
+        }
+        EV::template eval<T, 1>(in, a, v);
+        if (out) out[j * a.out_ld + r0 + i] = v[0];
+        acc.template add_at<1>(v, e0 + i);
+      };
+      for (u64 i = threadIdx.x; i < head; i += kConsumerWarps * 32) scalar_elem(i);
+      uint4* po = out ? reinterpret_cast<uint4*>(out + j * a.out_ld + r0 + head) : nullptr;
+      for (u64 u0 = 0; u0 < nun; u0 += TU) {
+        const uint32_t nu = (uint32_t)((nun - u0) < TU ? (nun - u0) : TU);
+        mbar_wait(&full[s], ph);
+        const unsigned char* stg = smem + (size_t)s * nk * tile_bytes;
+        for (uint32_t i = threadIdx.x; i < nu; i += UD * kConsumerWarps * 32) {
+          T v[UD * W];
+          EV::template eval_src<T, UD * W>(SmemSrc<T, UD>{stg + (size_t)i * 16, tile_bytes}, a, v);
+#pragma unroll
+          for (int q = 0; q < UD; ++q) {
+            const uint32_t iq = i + q * kConsumerWarps * 32;
+            if (q == 0 || iq < nu) {
+              T vq[W];
+#pragma unroll
+              for (int w = 0; w < W; ++w) vq[w] = v[q * W + w];
+              if (po) {
+                uint4 r;
+                memcpy(&r, &vq[0], 16);
+                st16(po + u0 + iq, r);
+              }
+              acc.template add_at<W>(vq, e0 + head + (u0 + iq) * W);
+            }
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+        if (++s == S) {
+          s = 0;
+          ph ^= 1u;
+        }
+      }
+      for (u64 i = head + nun * W + threadIdx.x; i < len; i += kConsumerWarps * 32) scalar_elem(i);
+    }
+  }
+  if constexpr (ACC != ACC_NONE) {
+    Accum<T, ACC> bt = block_reduce<T, ACC>(acc);
+    grid_finish<T, ACC>(bt, a.partials, a.ticket, a.final_mode, a.kind, a.result, a.count);
+  } else {
+    __syncthreads();  // the producer stays resident until every staged tile is consumed
   }
 }
 

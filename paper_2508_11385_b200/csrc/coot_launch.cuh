@@ -17,11 +17,13 @@ typedef void (*DimFn)(const DimArgs);
 // ahead) so every thread keeps >= 64 bytes of loads in flight.
 constexpr int unroll_for(int k) { return k <= 1 ? 4 : (k == 2 ? 2 : 1); }
 
-// driver: 0 = LDG, 1 = TMA-staged, 2 = strided views (interpreter only)
+// driver: 0 = LDG, 1 = TMA-staged, 2 = strided views, 3 = contiguous-column views
+// (2 and 3: interpreter only)
 template <class T, int ACC, class EV, int U>
 FusedFn driver_kernel(int driver) {
   if constexpr (EV::kInterp) {
     if (driver == 2) return &fused_strided_kernel<T, ACC, EV>;
+    if (driver == 3) return &fused_cols_tma_kernel<T, ACC, EV>;
   }
   if (driver == 1) return &fused_tma_kernel<T, ACC, EV>;
   return &fused_kernel<T, ACC, EV, U>;
@@ -30,7 +32,7 @@ FusedFn driver_kernel(int driver) {
 template <class T, int ACC, int... Code>
 FusedFn catalog_kernel(int driver) {
   typedef StaticProg<Code...> P;
-  if (driver == 2) return nullptr;  // views always run on the interpreter
+  if (driver >= 2) return nullptr;  // views always run on the interpreter
   if constexpr (P::template legal<T>()) {
     return driver_kernel<T, ACC, CatalogEval<P>, unroll_for(P::n_ops())>(driver);
   } else {
@@ -94,7 +96,7 @@ template <class T>
 cudaError_t launch_fused_t(const FusedPlan& p, const FusedArgs& a, cudaStream_t s) {
   FusedFn k = pick_fused<T>(p);
   if (!k) return cudaErrorInvalidDeviceFunction;
-  if (p.driver == 1) {
+  if (p.driver == 1 || p.driver == 3) {
     cudaError_t e = allow_smem(reinterpret_cast<const void*>(k), p.smem);
     if (e != cudaSuccess) return e;
     k<<<p.grid, kTmaThreads, p.smem, s>>>(a);

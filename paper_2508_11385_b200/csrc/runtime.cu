@@ -451,6 +451,39 @@ coot_status run_strided(coot_ctx* ctx, const coot_expr* e, const Shape& sh, int 
   p.acc = acc;
   p.grid = (unsigned)std::max<u64>(
       1, std::min<u64>(ceil_div(n, coot::kThreads), (u64)ctx->sm_count * ctx->blocks_per_sm));
+  // Contiguous columns (inc == 1 everywhere) with one shared 16-byte column
+  // misalignment: stream each column through the TMA ring (driver 3).
+  const size_t es = elem_size(e->elem);
+  const u64 m = e->n_rows;
+  const uintptr_t mis = reinterpret_cast<uintptr_t>(e->operands[0].ptr) & 15;
+  bool cols = ctx->driver == 1 && m >= 64;
+  for (uint32_t k = 0; k < e->n_operands && cols; ++k) {
+    const coot_operand& o = e->operands[k];
+    cols = op_inc(o) == 1 && ((op_ld(o) * es) % 16 == 0 || e->n_cols == 1) &&
+           (reinterpret_cast<uintptr_t>(o.ptr) & 15) == mis;
+  }
+  if (cols && a.out)
+    cols = a.out_inc == 1 && ((a.out_ld * es) % 16 == 0 || e->n_cols == 1) &&
+           (reinterpret_cast<uintptr_t>(a.out) & 15) == mis;
+  if (cols) {
+    const u64 G = (u64)ctx->sm_count * ctx->tma_ctas_per_sm;
+    const u64 nk = e->n_operands;
+    const u64 tile_el = (u64)coot::kTileUnits * (16 / es);
+    u64 S = std::max<u64>(1, ceil_div(8 * G, e->n_cols));
+    S = std::min<u64>(S, std::max<u64>(1, m / tile_el));
+    const u64 L = ceil_div(ceil_div(m, S), tile_el) * tile_el;
+    S = ceil_div(m, L);
+    const u64 stage_bytes = nk * coot::kTileUnits * 16;
+    const u64 stages = std::max<u64>(2, std::min<u64>(8, (96u << 10) / stage_bytes));
+    a.ncols = e->n_cols;
+    a.seg_len = L;
+    a.nseg = (uint32_t)S;
+    a.tile_units = coot::kTileUnits;
+    a.stages = (uint32_t)stages;
+    p.driver = 3;
+    p.smem = (unsigned)(stages * stage_bytes + 16 * stages);
+    p.grid = (unsigned)std::max<u64>(1, std::min<u64>(e->n_cols * S, G));
+  }
   if (ctx->log)
     fprintf(stderr, "[coot] strided elem=%u %llux%llu acc=%d grid=%u\n", e->elem,
             (unsigned long long)e->n_rows, (unsigned long long)e->n_cols, acc, p.grid);

@@ -124,6 +124,45 @@ def test_sum_dim_over_views(coot, ctx, etype, dim):
         assert_reduction(got[i], want[i], etype, "ACCU", 1.0)
 
 
+@pytest.mark.parametrize("etype", ALL)
+@pytest.mark.parametrize("r0", [4, 1])  # 16-byte aligned columns / shared misalignment
+def test_contiguous_column_views_tma_path(coot, ctx, etype, r0):
+    """Submatrix views whose columns share one misalignment (incl. the
+    destination) take the column-streaming TMA path; results must match."""
+    m, n = 1024, 512
+    A, HA = dev_mat(coot, etype, m, n, 6)
+    B, HB = dev_mat(coot, etype, m, n, 7)
+    Z, HZ = dev_mat(coot, etype, m, n, 8)
+    a = A.submat(r0, 3, r0 + 999, 402)     # 1000 x 400
+    b = B.submat(r0 + 16, 50, r0 + 1015, 449)
+    z = Z.submat(r0 + 8, 100, r0 + 1007, 499)
+    sa = HA[r0:r0 + 1000, 3:403].T.reshape(-1)
+    sb = HB[r0 + 16:r0 + 1016, 50:450].T.reshape(-1)
+    prog = P("S0 L0 MUL L1 ADD")
+    want = oracle.eval_program(etype, prog, [sa, sb], [3])
+    z.assign(3 * a + b)
+    torch.cuda.synchronize()
+    got = to_host(Z.data, etype).reshape(n, m).T
+    assert np.array_equal(got[r0 + 8:r0 + 1008, 100:500].T.reshape(-1), want)
+    keep = np.ones_like(HZ, dtype=bool)
+    keep[r0 + 8:r0 + 1008, 100:500] = False
+    assert np.array_equal(got[keep], HZ[keep])
+    for kind in ["ACCU", "MINMAX", "INDEX_MAX"] + (["VAR"] if etype in FLOATS else []):
+        fn = {"ACCU": coot.accu, "MINMAX": coot.minmax, "INDEX_MAX": coot.index_max,
+              "VAR": coot.var}[kind]
+        r = fn(3 * a + b, ctx)
+        torch.cuda.synchronize()
+        if kind == "INDEX_MAX":
+            assert int(r[0].item()) == oracle.stats(etype, kind, want)
+        elif kind == "VAR":
+            assert_reduction(to_host(r, etype)[0], oracle.stats(etype, kind, want), etype, "ACCU")
+        else:
+            g = to_host(r, etype)
+            g = g[:2] if kind == "MINMAX" else g[0]
+            assert_reduction(g, oracle.reduce(etype, kind, want), etype, kind,
+                             float(np.abs(want.astype(np.float64)).sum()))
+
+
 def test_view_alias_rules(coot, ctx):
     m, n = 64, 64
     A, _ = dev_mat(coot, "f32", m, n, 5)

@@ -40,6 +40,12 @@ WL = {
     "c3_dim0": ("f64", 32768, 32768, "L0", [], "SUM_DIM0", False, False),
     "c3_dim1": ("f64", 32768, 32768, "L0", [], "SUM_DIM1", False, False),
     "c1_axpy_1e6": ("f32", 1_000_000, 1, "S0 L0 MUL L1 ADD", [2.5], "ACCU", True, False),
+    "mean_2p30": ("f32", 1 << 30, 1, "L0", [], "MEAN", False, False),
+    "var_2p30": ("f32", 1 << 30, 1, "L0", [], "VAR", False, False),
+    "var_f64_2p29": ("f64", 1 << 29, 1, "L0", [], "VAR", False, False),
+    "imin_2p30": ("f32", 1 << 30, 1, "L0", [], "INDEX_MIN", False, False),
+    "diag_add_1e4": ("f32", 10_000, 1, "L0 S0 ADD", [100.0], None, "diag", False),
+    "submat_axpy": ("f32", 8192, 8192, "S0 L0 MUL L1 ADD", [2.5], "ACCU", "submat", False),
 }
 
 
@@ -49,15 +55,30 @@ def run(name, reps, ctxs):
     ctx = ctxs[1] if interp else ctxs[0]
     k = 1 + max(a for o, a in prog if o == "LOAD")
     dt = api.TORCH_DTYPE[elem]
-    ops = [torch.empty(m * n, dtype=dt, device="cuda") for _ in range(k)]
-    for s, t in enumerate(ops):
-        ctx.fill(t, "randu", stream=s, n_rows=m)
-    out = torch.empty(m * n, dtype=dt, device="cuda") if store else None
+    es = api.ESIZE[elem]
+    if store in ("diag", "submat"):  # strided views of 10000 x 10000 parents
+        P_ = 10000
+        parents = [torch.empty(P_ * P_, dtype=dt, device="cuda") for _ in range(k)]
+        for s, t in enumerate(parents):
+            ctx.fill(t, "randu", stream=s, n_rows=P_)
+        if store == "diag":
+            ops = [(t.data_ptr(), m, 1, m, P_ + 1) for t in parents]
+        else:
+            ops = [(t.data_ptr() + (100 + 200 * P_) * es, m, n, P_, 1) for t in parents]
+        out = None
+    else:
+        ops = [torch.empty(m * n, dtype=dt, device="cuda") for _ in range(k)]
+        for s, t in enumerate(ops):
+            ctx.fill(t, "randu", stream=s, n_rows=m)
+        out = torch.empty(m * n, dtype=dt, device="cuda") if store else None
     rlen = n if kind == "SUM_DIM0" else (m if kind == "SUM_DIM1" else 2)
-    res = torch.empty(rlen, dtype=dt, device="cuda")
+    res = torch.empty(rlen, dtype=torch.int64 if kind and kind.startswith("INDEX") else dt,
+                      device="cuda")
 
     def call():
-        if kind is None:
+        if store == "diag":
+            ctx.eval_view(elem, m, n, prog, ops, sc, ops[0])
+        elif kind is None:
             ctx.eval(elem, m, n, prog, ops, sc, out)
         else:
             ctx.reduce(elem, m, n, prog, ops, sc, kind, res, out)
@@ -72,11 +93,12 @@ def run(name, reps, ctxs):
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / reps
-    es = api.ESIZE[elem]
     rbytes = (n if kind == "SUM_DIM0" else m if kind == "SUM_DIM1" else 0) * es
-    alg = m * n * es * (k + (1 if store else 0)) + rbytes
+    alg = m * n * es * (k + (1 if store in (True, "diag") else 0)) + rbytes
     st = ctx.stats()
     del ops, out
+    if store in ("diag", "submat"):
+        del parents
     torch.cuda.empty_cache()
     return {"name": name, "ms": ms, "GBps": alg / ms / 1e6, "Gelem_s": m * n / ms / 1e6,
             "grid": st["last_grid"], "path": st["last_path"]}
