@@ -21,8 +21,22 @@ import numpy as np
 
 from . import build as _build
 
-TYPES = {"f32": 0, "f64": 1, "u32": 2, "s64": 3}
-DTYPES = {"f32": np.float32, "f64": np.float64, "u32": np.uint32, "s64": np.int64}
+TYPES = {"f32": 0, "f64": 1, "u32": 2, "s64": 3, "bf16": 4, "f16": 5}
+# bf16 arrays are carried as their uint16 bit patterns (numpy has no bfloat16)
+DTYPES = {"f32": np.float32, "f64": np.float64, "u32": np.uint32, "s64": np.int64,
+          "bf16": np.uint16, "f16": np.float16}
+
+
+def bf16_to_f32(bits: np.ndarray) -> np.ndarray:
+    """Exact widening of bf16 bit patterns to float32."""
+    return (np.asarray(bits, dtype=np.uint16).astype(np.uint32) << 16).view(np.float32)
+
+
+def to_float(etype: str, a: np.ndarray) -> np.ndarray:
+    """Exact float64 values of an array of any float element type."""
+    if etype == "bf16":
+        return bf16_to_f32(a).astype(np.float64)
+    return np.asarray(a).astype(np.float64)
 OPS = {
     "LOAD": 0, "SCALAR": 1, "NEG": 2, "ABS": 3, "SQUARE": 4, "SQRT": 5, "EXP": 6,
     "LOG": 7, "ADD": 8, "SUB": 9, "MUL": 10, "DIV": 11, "MIN": 12, "MAX": 13,
@@ -39,6 +53,8 @@ def lib():
         path = _build.build()
         L = ctypes.CDLL(path)
         u64, i32, vp = ctypes.c_uint64, ctypes.c_int, ctypes.c_void_p
+        L.orc_half_from_double.restype = ctypes.c_uint16
+        L.orc_half_from_double.argtypes = [i32, ctypes.c_double]
         L.orc_hash.restype = u64
         L.orc_hash.argtypes = [u64, u64, u64]
         L.orc_fill.restype = i32
@@ -101,7 +117,15 @@ def _encode_program(program):
 
 
 def _scalar_array(etype: str, scalars):
+    if etype in ("bf16", "f16"):  # R4: the scalar rounded once to the 16-bit format
+        bits = [lib().orc_half_from_double(TYPES[etype], float(s)) for s in (scalars or [0])]
+        return np.array(bits, dtype=np.uint16).view(DTYPES[etype])
     return np.array(list(scalars) if scalars else [0], dtype=DTYPES[etype])
+
+
+def half_from_double(etype: str, x: float) -> int:
+    """Bits of x rounded (nearest-even) to bf16 / f16."""
+    return int(lib().orc_half_from_double(TYPES[etype], float(x)))
 
 
 def eval_program(etype: str, program, operands, scalars=()) -> np.ndarray:

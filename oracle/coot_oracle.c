@@ -35,7 +35,9 @@
 #include <string.h>
 
 /* ---- element types and opcodes (the oracle's own numbering) ------------ */
-enum { ORC_F32 = 0, ORC_F64 = 1, ORC_U32 = 2, ORC_S64 = 3 };
+/* BF16 / F16 (reading R24): 16-bit storage, every node rounded to the storage
+ * format; the roadmap's low-precision types. */
+enum { ORC_F32 = 0, ORC_F64 = 1, ORC_U32 = 2, ORC_S64 = 3, ORC_BF16 = 4, ORC_F16 = 5 };
 
 enum {
   ORC_LOAD = 0, ORC_SCALAR = 1,
@@ -56,9 +58,78 @@ static size_t esize(int type) {
     case ORC_F64: return 8;
     case ORC_U32: return 4;
     case ORC_S64: return 8;
+    case ORC_BF16: return 2;
+    case ORC_F16: return 2;
   }
   return 0;
 }
+
+static int is_half(int type) { return type == ORC_BF16 || type == ORC_F16; }
+static int is_flt(int type) {
+  return type == ORC_F32 || type == ORC_F64 || is_half(type);
+}
+
+/* ---- 16-bit float formats ------------------------------------------------
+ * bf16: 1 sign, 8 exponent, 7 mantissa bits (bias 127);
+ * f16 (IEEE binary16): 1 sign, 5 exponent, 10 mantissa bits (bias 15).
+ * half_decode is exact; half_round rounds an exact __float128 value to the
+ * format with round-half-to-even (subnormals, overflow to inf), written out
+ * with integer arithmetic on the scaled significand. */
+static void fmt_of(int type, int* ebits, int* mbits) {
+  *ebits = type == ORC_BF16 ? 8 : 5;
+  *mbits = type == ORC_BF16 ? 7 : 10;
+}
+
+static double half_decode(int type, uint16_t b) {
+  int ebits, mbits;
+  fmt_of(type, &ebits, &mbits);
+  const int bias = (1 << (ebits - 1)) - 1;
+  const int sign = b >> 15;
+  const int e = (b >> mbits) & ((1 << ebits) - 1);
+  const int m = b & ((1 << mbits) - 1);
+  double v;
+  if (e == (1 << ebits) - 1) v = m ? NAN : INFINITY;
+  else if (e == 0) v = ldexp((double)m, 1 - bias - mbits);
+  else v = ldexp((double)(m | (1 << mbits)), e - bias - mbits);
+  return sign ? -v : v;
+}
+
+static uint16_t half_round(int type, __float128 x) {
+  int ebits, mbits;
+  fmt_of(type, &ebits, &mbits);
+  const int bias = (1 << (ebits - 1)) - 1;
+  const uint16_t emask = (uint16_t)(((1 << ebits) - 1) << mbits);
+  if (isnanq(x)) return (uint16_t)(emask | (1u << (mbits - 1)));
+  const uint16_t sign = signbitq(x) ? 0x8000 : 0;
+  __float128 a = fabsq(x);
+  if (isinfq(a)) return (uint16_t)(sign | emask);
+  if (a == 0) return sign;
+  int k;
+  frexpq(a, &k);               /* a = f * 2^k, f in [0.5, 1) */
+  int E = k - 1;               /* 2^E <= a < 2^(E+1) */
+  const int emin = 1 - bias;
+  const int qe = (E < emin ? emin : E) - mbits;  /* exponent of one ulp */
+  const __float128 scaled = ldexpq(a, -qe);       /* exact */
+  uint64_t n = (uint64_t)floorq(scaled);
+  const __float128 rem = scaled - (__float128)n;
+  if (rem > 0.5Q || (rem == 0.5Q && (n & 1))) ++n;
+  /* n * 2^qe is the rounded magnitude */
+  int field;
+  uint64_t mant;
+  if (n < (1ull << mbits)) {   /* subnormal (or rounded up to the smallest normal below) */
+    field = 0;
+    mant = n;
+  } else {
+    int eq = qe;
+    if (n == (2ull << mbits)) { n >>= 1; ++eq; }
+    field = eq + mbits + bias;
+    mant = n - (1ull << mbits);
+    if (field >= (1 << ebits) - 1) return (uint16_t)(sign | emask);  /* overflow */
+  }
+  return (uint16_t)(sign | ((uint16_t)field << mbits) | (uint16_t)mant);
+}
+
+uint16_t orc_half_from_double(int type, double x) { return half_round(type, (__float128)x); }
 
 /* ---- input generator ----------------------------------------------------
  * mix(z): SplitMix64 finaliser (Vigna, splitmix64.c).
@@ -100,6 +171,9 @@ static void fill_one(int type, int kind, uint64_t seed, uint64_t stream,
       case ORC_F64: ((double*)out)[idx] = (double)(h >> 11) * 0x1p-53; break;
       case ORC_U32: ((uint32_t*)out)[idx] = (uint32_t)(h >> 32); break;
       case ORC_S64: ((int64_t*)out)[idx] = (int64_t)h; break;
+      /* uniform [0,1) on the format's significand grid (exactly representable) */
+      case ORC_BF16: ((uint16_t*)out)[idx] = half_round(type, (__float128)(h >> 56) * 0x1p-8Q); break;
+      case ORC_F16: ((uint16_t*)out)[idx] = half_round(type, (__float128)(h >> 53) * 0x1p-11Q); break;
     }
   } else {
     switch (type) {
@@ -107,6 +181,8 @@ static void fill_one(int type, int kind, uint64_t seed, uint64_t stream,
       case ORC_F64: ((double*)out)[idx] = (double)iv; break;
       case ORC_U32: ((uint32_t*)out)[idx] = (uint32_t)iv; break;
       case ORC_S64: ((int64_t*)out)[idx] = (int64_t)iv; break;
+      case ORC_BF16:
+      case ORC_F16: ((uint16_t*)out)[idx] = half_round(type, (__float128)iv); break;
     }
   }
 }
@@ -220,6 +296,38 @@ static uint64_t s64_bin(int op, uint64_t a, uint64_t b) {
   return 0;
 }
 
+/* bf16 / f16 (reading R24): the exact value of the node, rounded once to the
+ * 16-bit format.  + - * / sqrt are computed in binary64 — exact or correctly
+ * rounded there, and 53 >= 2p + 2 for p = 8 (bf16) and p = 11 (f16), so the
+ * second rounding to the format is still the correctly rounded result
+ * (Figueroa's double-rounding theorem); exp/log in binary128.  NEG / ABS flip
+ * or clear the sign bit; MIN / MAX return one of the inputs. */
+static uint16_t h_un(int type, int op, uint16_t a) {
+  const double x = half_decode(type, a);
+  switch (op) {
+    case ORC_NEG: return (uint16_t)(a ^ 0x8000);
+    case ORC_ABS: return (uint16_t)(a & 0x7fff);
+    case ORC_SQUARE: return half_round(type, (__float128)(x * x));
+    case ORC_SQRT: return half_round(type, (__float128)sqrt(x));
+    case ORC_EXP: return half_round(type, expq((__float128)x));
+    case ORC_LOG: return half_round(type, logq((__float128)x));
+  }
+  return 0;
+}
+
+static uint16_t h_bin(int type, int op, uint16_t a, uint16_t b) {
+  const double x = half_decode(type, a), y = half_decode(type, b);
+  switch (op) {
+    case ORC_ADD: return half_round(type, (__float128)(x + y));
+    case ORC_SUB: return half_round(type, (__float128)(x - y));
+    case ORC_MUL: return half_round(type, (__float128)(x * y));
+    case ORC_DIV: return half_round(type, (__float128)(x / y));
+    case ORC_MIN: return (y < x) ? b : a;
+    case ORC_MAX: return (x < y) ? b : a;
+  }
+  return 0;
+}
+
 static int is_unary(int op) { return op >= ORC_NEG && op <= ORC_LOG; }
 static int is_binary(int op) { return op >= ORC_ADD && op <= ORC_MAX; }
 static int legal_for(int type, int op) {
@@ -236,6 +344,8 @@ static void apply_unary(int type, int op, uint64_t n, const void* a, void* dst) 
       case ORC_F64: ((double*)dst)[i] = f64_un(op, ((const double*)a)[i]); break;
       case ORC_U32: ((uint32_t*)dst)[i] = u32_un(op, ((const uint32_t*)a)[i]); break;
       case ORC_S64: ((uint64_t*)dst)[i] = s64_un(op, ((const uint64_t*)a)[i]); break;
+      case ORC_BF16:
+      case ORC_F16: ((uint16_t*)dst)[i] = h_un(type, op, ((const uint16_t*)a)[i]); break;
     }
   }
 }
@@ -255,6 +365,10 @@ static void apply_binary(int type, int op, uint64_t n, const void* a, const void
         break;
       case ORC_S64:
         ((uint64_t*)dst)[i] = s64_bin(op, ((const uint64_t*)a)[i], ((const uint64_t*)b)[i]);
+        break;
+      case ORC_BF16:
+      case ORC_F16:
+        ((uint16_t*)dst)[i] = h_bin(type, op, ((const uint16_t*)a)[i], ((const uint16_t*)b)[i]);
         break;
     }
   }
@@ -362,7 +476,17 @@ static void neumaier(long double* s, long double* c, long double x) {
 
 static long double elem_as_ld(int type, const void* v, uint64_t i) {
   if (type == ORC_F32) return (long double)((const float*)v)[i];
+  if (is_half(type)) return (long double)half_decode(type, ((const uint16_t*)v)[i]);
   return (long double)((const double*)v)[i];
+}
+
+/* Round an exact-ish binary128 value once to the float type and store it. */
+static void store_flt(int type, void* out, size_t idx, __float128 r) {
+  switch (type) {
+    case ORC_F32: ((float*)out)[idx] = (float)r; break;
+    case ORC_F64: ((double*)out)[idx] = (double)r; break;
+    default: ((uint16_t*)out)[idx] = half_round(type, r); break;
+  }
 }
 
 static uint64_t elem_as_u64(int type, const void* v, uint64_t i) {
@@ -378,7 +502,7 @@ static int int_less(int type, uint64_t a, uint64_t b) {
 int orc_acc_add(orc_acc* a, uint64_t n, const void* v) {
   int type = a->type;
   for (uint64_t i = 0; i < n; ++i) {
-    if (type == ORC_F32 || type == ORC_F64) {
+    if (is_flt(type)) {
       long double x = elem_as_ld(type, v, i);
       switch (a->kind) {
         case ORC_ACCU: neumaier(&a->s, &a->c, x); break;
@@ -420,32 +544,18 @@ int orc_acc_final(const orc_acc* a, void* result) {
   int type = a->type;
   if ((a->kind == ORC_RMIN || a->kind == ORC_RMAX || a->kind == ORC_MINMAX) && a->count == 0)
     return ORC_E_EMPTY;
-  if (type == ORC_F32 || type == ORC_F64) {
-    double r0 = 0, r1 = 0;
-    int two = 0;
+  if (is_flt(type)) {
     switch (a->kind) {
-      case ORC_ACCU:
-        if (type == ORC_F32) { ((float*)result)[0] = (float)acc_total(a); return ORC_E_OK; }
-        ((double*)result)[0] = (double)acc_total(a);
+      case ORC_ACCU: store_flt(type, result, 0, acc_total(a)); return ORC_E_OK;
+      case ORC_NORM2: store_flt(type, result, 0, sqrtq(acc_total(a))); return ORC_E_OK;
+      case ORC_RMIN: store_flt(type, result, 0, (__float128)a->fmin); return ORC_E_OK;
+      case ORC_RMAX: store_flt(type, result, 0, (__float128)a->fmax); return ORC_E_OK;
+      case ORC_MINMAX:  /* extremes are elements: exactly representable */
+        store_flt(type, result, 0, (__float128)a->fmin);
+        store_flt(type, result, 1, (__float128)a->fmax);
         return ORC_E_OK;
-      case ORC_NORM2: {
-        __float128 r = sqrtq(acc_total(a));
-        if (type == ORC_F32) ((float*)result)[0] = (float)r;
-        else ((double*)result)[0] = (double)r;
-        return ORC_E_OK;
-      }
-      case ORC_RMIN: r0 = a->fmin; break;
-      case ORC_RMAX: r0 = a->fmax; break;
-      case ORC_MINMAX: r0 = a->fmin; r1 = a->fmax; two = 1; break;
     }
-    if (type == ORC_F32) {
-      ((float*)result)[0] = (float)r0;
-      if (two) ((float*)result)[1] = (float)r1;
-    } else {
-      ((double*)result)[0] = r0;
-      if (two) ((double*)result)[1] = r1;
-    }
-    return ORC_E_OK;
+    return ORC_E_KIND;
   }
   uint64_t r0 = 0, r1 = 0;
   int two = 0;
@@ -507,6 +617,12 @@ int orc_stats(int type, int kind, uint64_t n, const void* v, void* result) {
           better = kind == ORC_IMIN ? (a < b) : (a > b);
           break;
         }
+        case ORC_BF16:
+        case ORC_F16: {
+          double a = (double)elem_as_ld(type, v, i), b = (double)elem_as_ld(type, v, best);
+          better = kind == ORC_IMIN ? (a < b) : (a > b);
+          break;
+        }
         default: {
           int64_t a = ((const int64_t*)v)[i], b = ((const int64_t*)v)[best];
           better = kind == ORC_IMIN ? (a < b) : (a > b);
@@ -518,7 +634,7 @@ int orc_stats(int type, int kind, uint64_t n, const void* v, void* result) {
     *(uint64_t*)result = best;
     return ORC_E_OK;
   }
-  if (type != ORC_F32 && type != ORC_F64) return ORC_E_KIND;
+  if (!is_flt(type)) return ORC_E_KIND;
   if (kind < ORC_MEAN || kind > ORC_STDDEV) return ORC_E_KIND;
   if (n == 0) return ORC_E_EMPTY;
   long double s = 0, c = 0;
@@ -537,8 +653,7 @@ int orc_stats(int type, int kind, uint64_t n, const void* v, void* result) {
     r = n > 1 ? ((__float128)s2 + (__float128)c2) / (__float128)(n - 1) : (__float128)0;
     if (kind == ORC_STDDEV) r = sqrtq(r);
   }
-  if (type == ORC_F32) *(float*)result = (float)r;
-  else *(double*)result = (double)r;
+  store_flt(type, result, 0, r);
   return ORC_E_OK;
 }
 
@@ -553,7 +668,7 @@ int orc_stats(int type, int kind, uint64_t n, const void* v, void* result) {
 int orc_sum_dim(int type, int dim, uint64_t m, uint64_t n, const void* X, void* out) {
   size_t es = esize(type);
   if (es == 0) return ORC_E_TYPE;
-  int is_float = (type == ORC_F32 || type == ORC_F64);
+  int is_float = is_flt(type);
   if (dim == 0) {
     for (uint64_t j = 0; j < n; ++j) {
       orc_acc a;
@@ -589,6 +704,8 @@ int orc_sum_dim(int type, int dim, uint64_t m, uint64_t n, const void* X, void* 
       case ORC_F64: ((double*)out)[i] = (double)((__float128)s[i] + (__float128)c[i]); break;
       case ORC_U32: ((uint32_t*)out)[i] = (uint32_t)u[i]; break;
       case ORC_S64: ((uint64_t*)out)[i] = u[i]; break;
+      case ORC_BF16:
+      case ORC_F16: store_flt(type, out, i, (__float128)s[i] + (__float128)c[i]); break;
     }
   }
   free(s);

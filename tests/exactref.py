@@ -17,7 +17,8 @@ import mpmath
 import numpy as np
 
 # (precision incl. hidden bit, emin, emax)
-FMT = {"f32": (24, -126, 127), "f64": (53, -1022, 1023)}
+FMT = {"f32": (24, -126, 127), "f64": (53, -1022, 1023), "bf16": (8, -126, 127),
+       "f16": (11, -14, 15)}
 MASK = {"u32": (1 << 32) - 1, "s64": (1 << 64) - 1}
 
 
