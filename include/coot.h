@@ -53,7 +53,12 @@ extern "C" {
 #define COOT_MAX_STACK 8    /* evaluation stack depth        */
 #define COOT_PARTIAL_BYTES 32u /* one scalar reduction partial record */
 
-typedef enum { COOT_F32 = 0, COOT_F64 = 1, COOT_U32 = 2, COOT_S64 = 3 } coot_elem_t;
+/* BF16 / F16: 16-bit float storage (the roadmap's low precision, P:596-603;
+ * R24): every node is computed exactly or in f32/f64 and rounded once to the
+ * 16-bit format; reductions accumulate in f64 and round once. */
+typedef enum {
+  COOT_F32 = 0, COOT_F64 = 1, COOT_U32 = 2, COOT_S64 = 3, COOT_BF16 = 4, COOT_F16 = 5
+} coot_elem_t;
 
 typedef enum {
   COOT_OK = 0,
@@ -95,6 +100,7 @@ typedef union {
   double f64;
   uint32_t u32;
   int64_t s64;
+  uint16_t h16;  /* bf16 / f16 bit pattern */
   uint64_t bits;
 } coot_scalar;
 

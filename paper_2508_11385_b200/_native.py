@@ -20,7 +20,7 @@ MAX_INSTR = 32
 MAX_STACK = 8
 PARTIAL_BYTES = 32
 
-ELEM = {"f32": 0, "f64": 1, "u32": 2, "s64": 3}
+ELEM = {"f32": 0, "f64": 1, "u32": 2, "s64": 3, "bf16": 4, "f16": 5}
 OP = {"LOAD": 0, "SCALAR": 1, "NEG": 2, "ABS": 3, "SQUARE": 4, "SQRT": 5, "EXP": 6, "LOG": 7,
       "ADD": 8, "SUB": 9, "MUL": 10, "DIV": 11, "MIN": 12, "MAX": 13}
 KIND = {"ACCU": 0, "MIN": 1, "MAX": 2, "MINMAX": 3, "NORM2": 4, "SUM_DIM0": 5, "SUM_DIM1": 6,
@@ -157,12 +157,51 @@ def make_expr(elem: str, n_rows: int, n_cols: int, program, operands, scalars=()
     return e
 
 
+HALF_FMT = {"bf16": (8, 7), "f16": (5, 10)}  # (exponent bits, stored mantissa bits)
+
+
+def half_bits(value: float, elem: str) -> int:
+    """value rounded to nearest-even in bf16 / f16, as its 16-bit pattern."""
+    import math
+    from fractions import Fraction
+    ebits, mbits = HALF_FMT[elem]
+    bias = (1 << (ebits - 1)) - 1
+    emask = ((1 << ebits) - 1) << mbits
+    x = float(value)
+    if math.isnan(x):
+        return emask | (1 << (mbits - 1))
+    sign = 0x8000 if math.copysign(1.0, x) < 0 else 0
+    a = abs(x)
+    if math.isinf(a):
+        return sign | emask
+    if a == 0:
+        return sign
+    e = math.frexp(a)[1] - 1                 # 2^e <= a < 2^(e+1)
+    qe = max(e, 1 - bias) - mbits            # exponent of one unit in the last place
+    scaled = Fraction(a) / (Fraction(2) ** qe)
+    n = scaled.numerator // scaled.denominator
+    rem = scaled - n
+    if rem > Fraction(1, 2) or (rem == Fraction(1, 2) and n % 2 == 1):
+        n += 1
+    if n < (1 << mbits):
+        return sign | n                      # subnormal
+    if n == (2 << mbits):
+        n >>= 1
+        qe += 1
+    field = qe + mbits + bias
+    if field >= (1 << ebits) - 1:
+        return sign | emask                  # overflow
+    return sign | (field << mbits) | (n - (1 << mbits))
+
+
 def set_scalar(slot: Scalar, elem: str, value):
     """Store a scalar AS the element type (R4); reject lossy integer scalars."""
     if elem == "f32":
         slot.f32 = float(value)
     elif elem == "f64":
         slot.f64 = float(value)
+    elif elem in HALF_FMT:
+        slot.bits = half_bits(value, elem)
     else:
         if isinstance(value, float) and not value.is_integer():
             raise CootError(5, f"contract: scalar {value!r} is not integral for a {elem} expression")

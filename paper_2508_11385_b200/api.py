@@ -24,9 +24,9 @@ from . import _native as N
 from ._native import CootError, check, lib
 
 TORCH_DTYPE = {"f32": torch.float32, "f64": torch.float64, "u32": torch.uint32,
-               "s64": torch.int64}
+               "s64": torch.int64, "bf16": torch.bfloat16, "f16": torch.float16}
 ELEM_OF = {v: k for k, v in TORCH_DTYPE.items()}
-ESIZE = {"f32": 4, "f64": 8, "u32": 4, "s64": 8}
+ESIZE = {"f32": 4, "f64": 8, "u32": 4, "s64": 8, "bf16": 2, "f16": 2}
 
 
 def elem_of(t: torch.Tensor) -> str:

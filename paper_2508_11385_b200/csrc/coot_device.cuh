@@ -13,6 +13,8 @@
 //    accumulated in f64; the final value is rounded once to eT;
 //  * integers: modular (u64 accumulator, truncated at the end).
 #pragma once
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -22,6 +24,22 @@ namespace coot {
 
 typedef long long s64;
 typedef unsigned long long u64;
+
+// 16-bit float storage types (R24): a value is its bit pattern; every op
+// widens to f32 (exact), computes with IEEE round-to-nearest and rounds once
+// back (correctly rounded: 24 >= 2p + 2 for p = 8 and 11).  T(0) is +0.
+struct bf16 {
+  uint16_t bits;
+  __host__ __device__ constexpr bf16() : bits(0) {}
+  __host__ __device__ constexpr explicit bf16(int) : bits(0) {}
+  __host__ __device__ constexpr bf16(unsigned short b, bool) : bits(b) {}
+};
+struct f16 {
+  uint16_t bits;
+  __host__ __device__ constexpr f16() : bits(0) {}
+  __host__ __device__ constexpr explicit f16(int) : bits(0) {}
+  __host__ __device__ constexpr f16(unsigned short b, bool) : bits(b) {}
+};
 
 enum AccKind {
   ACC_NONE = 0, ACC_SUM = 1, ACC_SUMSQ = 2, ACC_MINMAX = 3,
@@ -92,6 +110,14 @@ template <>
 __device__ __forceinline__ s64 scalar_as<s64>(u64 bits) {
   return (s64)bits;
 }
+template <>
+__device__ __forceinline__ bf16 scalar_as<bf16>(u64 bits) {
+  return bf16((unsigned short)bits, true);
+}
+template <>
+__device__ __forceinline__ f16 scalar_as<f16>(u64 bits) {
+  return f16((unsigned short)bits, true);
+}
 
 template <class T>
 __device__ __forceinline__ u64 to_bits(T v);
@@ -111,10 +137,90 @@ template <>
 __device__ __forceinline__ u64 to_bits<s64>(s64 v) {
   return (u64)v;
 }
+template <>
+__device__ __forceinline__ u64 to_bits<bf16>(bf16 v) {
+  return (u64)v.bits;
+}
+template <>
+__device__ __forceinline__ u64 to_bits<f16>(f16 v) {
+  return (u64)v.bits;
+}
 
 template <class T>
+struct FloatTrait {
+  static constexpr bool value = false;
+  static constexpr bool half = false;
+};
+template <>
+struct FloatTrait<float> {
+  static constexpr bool value = true;
+  static constexpr bool half = false;
+};
+template <>
+struct FloatTrait<double> {
+  static constexpr bool value = true;
+  static constexpr bool half = false;
+};
+template <>
+struct FloatTrait<bf16> {
+  static constexpr bool value = true;
+  static constexpr bool half = true;
+};
+template <>
+struct FloatTrait<f16> {
+  static constexpr bool value = true;
+  static constexpr bool half = true;
+};
+template <class T>
 __host__ __device__ constexpr bool is_float() {
-  return T(0.5) != T(0);
+  return FloatTrait<T>::value;
+}
+template <class T>
+__host__ __device__ constexpr bool is_half() {
+  return FloatTrait<T>::half;
+}
+
+// ---- 16-bit conversions: widening is exact; narrowing rounds once (RNE) --------
+__device__ __forceinline__ float to_f32(bf16 v) { return __uint_as_float((unsigned)v.bits << 16); }
+__device__ __forceinline__ float to_f32(f16 v) { return __half2float(__ushort_as_half(v.bits)); }
+template <class H>
+__device__ __forceinline__ H half_from_f32(float x);
+template <>
+__device__ __forceinline__ bf16 half_from_f32<bf16>(float x) {
+  return bf16(__bfloat16_as_ushort(__float2bfloat16_rn(x)), true);
+}
+template <>
+__device__ __forceinline__ f16 half_from_f32<f16>(float x) {
+  return f16(__half_as_ushort(__float2half_rn(x)), true);
+}
+template <class H>
+__device__ __forceinline__ H half_from_f64(double x);
+template <>
+__device__ __forceinline__ bf16 half_from_f64<bf16>(double x) {
+  return bf16(__bfloat16_as_ushort(__double2bfloat16(x)), true);  // F2F.BF16.F64
+}
+template <>
+__device__ __forceinline__ f16 half_from_f64<f16>(double x) {
+  return f16(__half_as_ushort(__double2half(x)), true);  // F2F.F16.F64
+}
+// exact value of any element type as f64 (floats only are used)
+__device__ __forceinline__ double as_double(float v) { return (double)v; }
+__device__ __forceinline__ double as_double(double v) { return v; }
+__device__ __forceinline__ double as_double(bf16 v) { return (double)to_f32(v); }
+__device__ __forceinline__ double as_double(f16 v) { return (double)to_f32(v); }
+__device__ __forceinline__ double as_double(uint32_t v) { return (double)v; }
+__device__ __forceinline__ double as_double(s64 v) { return (double)v; }
+// ordering (IEEE semantics for floats)
+template <class T>
+__device__ __forceinline__ bool lt(T a, T b) {
+  if constexpr (is_half<T>()) return to_f32(a) < to_f32(b);
+  else return a < b;
+}
+// element loads bypassing L1 (operands may alias the output exactly)
+template <class T>
+__device__ __forceinline__ T ldcg_elem(const T* p) {
+  if constexpr (is_half<T>()) return T(__ldcg(reinterpret_cast<const unsigned short*>(p)), true);
+  else return __ldcg(p);
 }
 
 // ---- op legality (R9) -----------------------------------------------------
@@ -137,7 +243,7 @@ static __device__ const double kExp2Tab[64] = {
 #include "exp2_table.inc"
 };
 
-__device__ __forceinline__ float exp_f32_via_f64(float xf) {
+__device__ __forceinline__ double exp_f64_of_f32(float xf) {
   const float xc = fminf(fmaxf(xf, -104.0f), 89.0f);  // e^-104 < 2^-150 -> 0; e^89 -> inf
   const double x = (double)xc;
   const double kShift = 0x1.8p52;                            // 1.5 * 2^52: rint trick
@@ -156,8 +262,12 @@ __device__ __forceinline__ float exp_f32_via_f64(float xf) {
   const double t = __ldg(&kExp2Tab[ki & 63]);
   double y = __fma_rn(t, p, t);  // 2^(j/64) * e^r
   y = __longlong_as_double(__double_as_longlong(y) + ((long long)(ki >> 6) << 52));
-  const float res = __double2float_rn(y);
-  return (xf != xf) ? xf : res;  // NaN passes through
+  return (xf != xf) ? (double)xf : y;  // NaN passes through
+}
+
+// f32 / bf16 / f16 EXP: the f64 value above, rounded once to the format.
+__device__ __forceinline__ float exp_f32_via_f64(float xf) {
+  return __double2float_rn(exp_f64_of_f32(xf));
 }
 
 // ---- element semantics ------------------------------------------------------
@@ -186,6 +296,48 @@ __device__ __forceinline__ double un(double a) {
   else if constexpr (OP == COOT_OP_EXP) return exp(a);
   else if constexpr (OP == COOT_OP_LOG) return log(a);
   else return a;
+}
+// bf16 / f16 (R24): widen exactly, compute (f32 for + - * / sqrt, f64 for exp /
+// log), round once to the format.
+template <int OP, class H>
+__device__ __forceinline__ H half_un(H a) {
+  if constexpr (OP == COOT_OP_NEG) return H((unsigned short)(a.bits ^ 0x8000u), true);
+  else if constexpr (OP == COOT_OP_ABS) return H((unsigned short)(a.bits & 0x7fffu), true);
+  else {
+    const float x = to_f32(a);
+    if constexpr (OP == COOT_OP_SQUARE) return half_from_f32<H>(__fmul_rn(x, x));
+    else if constexpr (OP == COOT_OP_SQRT) return half_from_f32<H>(__fsqrt_rn(x));
+    else if constexpr (OP == COOT_OP_EXP) return half_from_f64<H>(exp_f64_of_f32(x));
+    else if constexpr (OP == COOT_OP_LOG) return half_from_f64<H>(log((double)x));
+    else return a;
+  }
+}
+template <int OP>
+__device__ __forceinline__ bf16 un(bf16 a) {
+  return half_un<OP, bf16>(a);
+}
+template <int OP>
+__device__ __forceinline__ f16 un(f16 a) {
+  return half_un<OP, f16>(a);
+}
+template <int OP, class H>
+__device__ __forceinline__ H half_bin(H a, H b) {
+  const float x = to_f32(a), y = to_f32(b);
+  if constexpr (OP == COOT_OP_ADD) return half_from_f32<H>(__fadd_rn(x, y));
+  else if constexpr (OP == COOT_OP_SUB) return half_from_f32<H>(__fsub_rn(x, y));
+  else if constexpr (OP == COOT_OP_MUL) return half_from_f32<H>(__fmul_rn(x, y));
+  else if constexpr (OP == COOT_OP_DIV) return half_from_f32<H>(__fdiv_rn(x, y));
+  else if constexpr (OP == COOT_OP_MIN) return (y < x) ? b : a;
+  else if constexpr (OP == COOT_OP_MAX) return (x < y) ? b : a;
+  else return a;
+}
+template <int OP>
+__device__ __forceinline__ bf16 bin(bf16 a, bf16 b) {
+  return half_bin<OP, bf16>(a, b);
+}
+template <int OP>
+__device__ __forceinline__ f16 bin(f16 a, f16 b) {
+  return half_bin<OP, f16>(a, b);
 }
 template <int OP>
 __device__ __forceinline__ uint32_t un(uint32_t a) {
@@ -344,6 +496,12 @@ __device__ __forceinline__ uint32_t shfl_xor(uint32_t v, int m) {
 __device__ __forceinline__ s64 shfl_xor(s64 v, int m) {
   return __shfl_xor_sync(0xffffffffu, v, m);
 }
+__device__ __forceinline__ bf16 shfl_xor(bf16 v, int m) {
+  return bf16((unsigned short)__shfl_xor_sync(0xffffffffu, (unsigned)v.bits, m), true);
+}
+__device__ __forceinline__ f16 shfl_xor(f16 v, int m) {
+  return f16((unsigned short)__shfl_xor_sync(0xffffffffu, (unsigned)v.bits, m), true);
+}
 
 // ---- per-thread accumulators -------------------------------------------------
 template <class T>
@@ -367,6 +525,16 @@ template <>
 struct MinMaxId<s64> {
   __device__ static s64 lo() { return 0x7fffffffffffffffll; }
   __device__ static s64 hi() { return (s64)0x8000000000000000ull; }
+};
+template <>
+struct MinMaxId<bf16> {
+  __device__ static bf16 lo() { return bf16(0x7f80, true); }  // +inf
+  __device__ static bf16 hi() { return bf16(0xff80, true); }  // -inf
+};
+template <>
+struct MinMaxId<f16> {
+  __device__ static f16 lo() { return f16(0x7c00, true); }
+  __device__ static f16 hi() { return f16(0xfc00, true); }
 };
 
 // Sum type: f64 for floats, u64 (modular) for integers.
@@ -396,9 +564,29 @@ __device__ __forceinline__ u64 sum_add<u64>(u64 a, u64 b) {
 
 // Pairwise sum of a unit (or one element) in eT, then widened.  For f32 the
 // unit of 4 is ((v0+v1)+(v2+v3)) in f32 — one f32->f64 conversion per unit.
+// Pairwise f32 sum of W (power of two) f32 values.
+template <int W>
+__device__ __forceinline__ float pairwise_f32(const float (&x)[W]) {
+  if constexpr (W == 1) {
+    return x[0];
+  } else {
+    float h[W / 2];
+#pragma unroll
+    for (int w = 0; w < W / 2; ++w) h[w] = __fadd_rn(x[2 * w], x[2 * w + 1]);
+    return pairwise_f32<W / 2>(h);
+  }
+}
+
 template <class T, int W>
 __device__ __forceinline__ typename SumT<T>::type unit_sum(const T (&v)[W]) {
-  if constexpr (is_float<T>()) {
+  if constexpr (is_half<T>()) {
+    // widen exactly, pairwise sum in f32 (error ~2^-24, far below the format's
+    // 2^-9 / 2^-12 rounding), one conversion to f64 per unit
+    float x[W];
+#pragma unroll
+    for (int w = 0; w < W; ++w) x[w] = to_f32(v[w]);
+    return (double)pairwise_f32<W>(x);
+  } else if constexpr (is_float<T>()) {
     if constexpr (W == 1) {
       return (double)v[0];
     } else if constexpr (W == 2) {
@@ -450,11 +638,11 @@ struct Accum {
       int bw = 0;
 #pragma unroll
       for (int w = 1; w < W; ++w) {
-        const bool better = (ACC == ACC_IMIN) ? (v[w] < bv) : (bv < v[w]);
+        const bool better = (ACC == ACC_IMIN) ? lt(v[w], bv) : lt(bv, v[w]);
         bv = better ? v[w] : bv;
         bw = better ? w : bw;
       }
-      const bool better = (ACC == ACC_IMIN) ? (bv < mn) : (mx < bv);
+      const bool better = (ACC == ACC_IMIN) ? lt(bv, mn) : lt(mx, bv);
       if (idx == ~0ull || better) {
         if constexpr (ACC == ACC_IMIN) mn = bv;
         else mx = bv;
@@ -467,11 +655,11 @@ struct Accum {
   template <int W>
   __device__ __forceinline__ void add(const T (&v)[W]) {
     if constexpr (ACC == ACC_VAR) {
-      if (n == 0) c = (double)v[0];  // the shift: the thread's first element
+      if (n == 0) c = as_double(v[0]);  // the shift: the thread's first element
       double a1 = 0.0, a2 = 0.0;     // the unit's shifted sums, then one update each
 #pragma unroll
       for (int w = 0; w < W; ++w) {
-        const double d = __dsub_rn((double)v[w], c);
+        const double d = __dsub_rn(as_double(v[w]), c);
         a1 = __dadd_rn(a1, d);
         a2 = __fma_rn(d, d, a2);
       }
@@ -481,10 +669,20 @@ struct Accum {
     } else if constexpr (ACC == ACC_SUM) {
       s = sum_add<S>(s, unit_sum<T, W>(v));
     } else if constexpr (ACC == ACC_SUMSQ) {
-      T q[W];
+      if constexpr (is_half<T>()) {  // squares of 16-bit values are exact in f32
+        float q[W];
 #pragma unroll
-      for (int w = 0; w < W; ++w) q[w] = bin<COOT_OP_MUL>(v[w], v[w]);
-      s = sum_add<S>(s, unit_sum<T, W>(q));
+        for (int w = 0; w < W; ++w) {
+          const float x = to_f32(v[w]);
+          q[w] = __fmul_rn(x, x);
+        }
+        s = sum_add<S>(s, (double)pairwise_f32<W>(q));
+      } else {
+        T q[W];
+#pragma unroll
+        for (int w = 0; w < W; ++w) q[w] = bin<COOT_OP_MUL>(v[w], v[w]);
+        s = sum_add<S>(s, unit_sum<T, W>(q));
+      }
     } else if constexpr (ACC == ACC_MINMAX) {
 #pragma unroll
       for (int w = 0; w < W; ++w) {
@@ -542,8 +740,8 @@ struct Accum {
     } else if constexpr (ACC == ACC_IMIN || ACC == ACC_IMAX) {
       if (o.idx == ~0ull) return;
       const T ov = ACC == ACC_IMIN ? o.mn : o.mx, v = ACC == ACC_IMIN ? mn : mx;
-      const bool better = ACC == ACC_IMIN ? (ov < v) : (v < ov);
-      if (idx == ~0ull || better || (!(v < ov) && !(ov < v) && o.idx < idx)) {
+      const bool better = ACC == ACC_IMIN ? lt(ov, v) : lt(v, ov);
+      if (idx == ~0ull || better || (!lt(v, ov) && !lt(ov, v) && o.idx < idx)) {
         mn = o.mn;
         mx = o.mx;
         idx = o.idx;
@@ -610,7 +808,8 @@ __device__ __forceinline__ Rec load_rec_cg(const Rec* p) {
 
 template <class T>
 __device__ __forceinline__ T round_to(double x) {
-  if constexpr (sizeof(T) == 4 && is_float<T>()) return __double2float_rn(x);
+  if constexpr (is_half<T>()) return half_from_f64<T>(x);
+  else if constexpr (sizeof(T) == 4 && is_float<T>()) return __double2float_rn(x);
   else return (T)x;
 }
 
@@ -640,12 +839,10 @@ __device__ __forceinline__ void write_final(const Accum<T, ACC>& acc, uint32_t k
       out[1] = acc.mx;
     }
   } else if constexpr (ACC == ACC_SUMSQ) {
-    if constexpr (sizeof(T) == 4) out[0] = __double2float_rn(__dsqrt_rn(acc.s));
-    else out[0] = (T)__dsqrt_rn(acc.s);
+    out[0] = round_to<T>(__dsqrt_rn(acc.s));
   } else if constexpr (ACC == ACC_SUM) {
     if constexpr (is_float<T>()) {
-      if constexpr (sizeof(T) == 4) out[0] = __double2float_rn(acc.s);
-      else out[0] = (T)acc.s;
+      out[0] = round_to<T>(acc.s);
     } else {
       out[0] = (T)acc.s;  // modular truncation for u32
     }

@@ -40,7 +40,7 @@ __device__ __forceinline__ void store_dim_value(const DimArgs& d, u64 idx,
     reinterpret_cast<S*>(d.result)[idx] = s;
   } else {
     T v;
-    if constexpr (sizeof(T) == 4 && is_float<T>()) v = __double2float_rn(s);
+    if constexpr (is_float<T>()) v = round_to<T>(s);
     else v = (T)s;
     reinterpret_cast<T*>(d.result)[idx] = v;
   }
@@ -156,7 +156,7 @@ __device__ __forceinline__ void load_elem_strided(const FusedArgs& a, u64 i, u64
 #pragma unroll
   for (int k = 0; k < EV::K; ++k) {
     if (!EV::kInterp || k < (int)a.n_operands)
-      in[k][0] = __ldcg(reinterpret_cast<const T*>(a.in[k]) + i * a.inc[k] + j * a.ld[k]);
+      in[k][0] = ldcg_elem(reinterpret_cast<const T*>(a.in[k]) + i * a.inc[k] + j * a.ld[k]);
     else
       in[k][0] = T(0);
   }

@@ -241,7 +241,7 @@ __device__ __forceinline__ void load_elem(const FusedArgs& a, u64 e, T (&in)[EV:
 #pragma unroll
   for (int k = 0; k < EV::K; ++k) {
     if (!EV::kInterp || k < (int)a.n_operands)
-      in[k][0] = __ldcg(reinterpret_cast<const T*>(a.in[k]) + e);
+      in[k][0] = ldcg_elem(reinterpret_cast<const T*>(a.in[k]) + e);
     else
       in[k][0] = T(0);
   }
@@ -349,7 +349,7 @@ __global__ void __launch_bounds__(kThreads) fused_strided_kernel(const __grid_co
 #pragma unroll
     for (int k = 0; k < K; ++k) {
       if (!EV::kInterp || k < (int)a.n_operands)
-        in[k][0] = __ldcg(reinterpret_cast<const T*>(a.in[k]) + i * a.inc[k] + j * a.ld[k]);
+        in[k][0] = ldcg_elem(reinterpret_cast<const T*>(a.in[k]) + i * a.inc[k] + j * a.ld[k]);
       else
         in[k][0] = T(0);
     }
@@ -593,7 +593,7 @@ __global__ void __launch_bounds__(kTmaThreads, tma_min_ctas<EV>())
 #pragma unroll
         for (int k = 0; k < K; ++k) {
           if (k < (int)nk)
-            in[k][0] = __ldcg(reinterpret_cast<const T*>(a.in[k]) + j * a.ld[k] + r0 + i);
+            in[k][0] = ldcg_elem(reinterpret_cast<const T*>(a.in[k]) + j * a.ld[k] + r0 + i);
           else
             in[k][0] = T(0);
         }

@@ -2,6 +2,7 @@
 // kernels_<type>.cu (so the four type families compile in parallel).
 #pragma once
 #include <mutex>
+#include <type_traits>
 #include <unordered_set>
 
 #include "coot_dim.cuh"
@@ -192,7 +193,7 @@ __global__ void combine_vec_kernel(const typename SumT<T>::type* parts, uint32_t
        i += (u64)gridDim.x * blockDim.x) {
     S s = S(0);
     for (uint32_t p = 0; p < nparts; ++p) s = sum_add<S>(s, parts[(u64)p * len + i]);
-    if constexpr (sizeof(T) == 4 && is_float<T>()) result[i] = __double2float_rn(s);
+    if constexpr (is_float<T>()) result[i] = round_to<T>(s);
     else result[i] = (T)s;
   }
 }
@@ -285,7 +286,9 @@ __global__ void fill_kernel(uint32_t kind, u64 seed, u64 stream, u64 start, u64 
     T v;
     if (kind == 0) {
       const u64 h = splitmix_mix(key + (g + 1) * 0x9E3779B97F4A7C15ull);
-      if constexpr (sizeof(T) == 4 && is_float<T>()) v = (float)(h >> 40) * 0x1p-24f;
+      if constexpr (std::is_same<T, bf16>::value) v = half_from_f32<bf16>((float)(h >> 56) * 0x1p-8f);
+      else if constexpr (std::is_same<T, f16>::value) v = half_from_f32<f16>((float)(h >> 53) * 0x1p-11f);
+      else if constexpr (sizeof(T) == 4 && is_float<T>()) v = (float)(h >> 40) * 0x1p-24f;
       else if constexpr (is_float<T>()) v = (double)(h >> 11) * 0x1p-53;
       else if constexpr (sizeof(T) == 4) v = (T)(h >> 32);
       else v = (T)h;
@@ -299,7 +302,8 @@ __global__ void fill_kernel(uint32_t kind, u64 seed, u64 stream, u64 start, u64 
         case 5: iv = g % n_rows; break;
         default: iv = 0; break;
       }
-      v = (T)iv;
+      if constexpr (is_half<T>()) v = half_from_f64<T>((double)iv);
+      else v = (T)iv;
     }
     out[i] = v;
   }

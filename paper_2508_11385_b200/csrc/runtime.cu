@@ -76,11 +76,15 @@ size_t elem_size(uint32_t elem) {
     case COOT_F64: return 8;
     case COOT_U32: return 4;
     case COOT_S64: return 8;
+    case COOT_BF16: return 2;
+    case COOT_F16: return 2;
   }
   return 0;
 }
 
-bool is_float_elem(uint32_t e) { return e == COOT_F32 || e == COOT_F64; }
+bool is_float_elem(uint32_t e) {
+  return e == COOT_F32 || e == COOT_F64 || e == COOT_BF16 || e == COOT_F16;
+}
 bool is_unary(int op) { return op >= COOT_OP_NEG && op <= COOT_OP_LOG; }
 bool is_binary(int op) { return op >= COOT_OP_ADD && op <= COOT_OP_MAX; }
 
@@ -358,6 +362,8 @@ cudaError_t dispatch_fused(uint32_t elem, const coot::FusedPlan& p, const coot::
     case COOT_F64: return coot::launch_fused_t<double>(p, a, s);
     case COOT_U32: return coot::launch_fused_t<uint32_t>(p, a, s);
     case COOT_S64: return coot::launch_fused_t<coot::s64>(p, a, s);
+    case COOT_BF16: return coot::launch_fused_t<coot::bf16>(p, a, s);
+    case COOT_F16: return coot::launch_fused_t<coot::f16>(p, a, s);
   }
   return cudaErrorInvalidValue;
 }
@@ -369,6 +375,8 @@ cudaError_t dispatch_dim(uint32_t elem, const coot::DimPlan& p, const coot::DimA
     case COOT_F64: return coot::launch_dim_t<double>(p, a, s);
     case COOT_U32: return coot::launch_dim_t<uint32_t>(p, a, s);
     case COOT_S64: return coot::launch_dim_t<coot::s64>(p, a, s);
+    case COOT_BF16: return coot::launch_dim_t<coot::bf16>(p, a, s);
+    case COOT_F16: return coot::launch_dim_t<coot::f16>(p, a, s);
   }
   return cudaErrorInvalidValue;
 }
@@ -772,6 +780,8 @@ coot_status reduce_common(coot_ctx* ctx, const coot_expr* e, uint32_t kind, void
         case COOT_F32: cerr = coot::launch_empty_rec_t<float>(acc, result, ctx->stream); break;
         case COOT_F64: cerr = coot::launch_empty_rec_t<double>(acc, result, ctx->stream); break;
         case COOT_U32: cerr = coot::launch_empty_rec_t<uint32_t>(acc, result, ctx->stream); break;
+        case COOT_BF16: cerr = coot::launch_empty_rec_t<coot::bf16>(acc, result, ctx->stream); break;
+        case COOT_F16: cerr = coot::launch_empty_rec_t<coot::f16>(acc, result, ctx->stream); break;
         default: cerr = coot::launch_empty_rec_t<coot::s64>(acc, result, ctx->stream); break;
       }
       if (cerr != cudaSuccess) return cuda_fail(cerr, "empty record launch");
@@ -962,6 +972,8 @@ coot_status coot_combine(coot_ctx* ctx, uint32_t elem, uint32_t kind, const void
     case COOT_F32: ce = coot::launch_combine_t<float>(kind, acc, partials, nparts, len, result, grid, ctx->stream); break;
     case COOT_F64: ce = coot::launch_combine_t<double>(kind, acc, partials, nparts, len, result, grid, ctx->stream); break;
     case COOT_U32: ce = coot::launch_combine_t<uint32_t>(kind, acc, partials, nparts, len, result, grid, ctx->stream); break;
+    case COOT_BF16: ce = coot::launch_combine_t<coot::bf16>(kind, acc, partials, nparts, len, result, grid, ctx->stream); break;
+    case COOT_F16: ce = coot::launch_combine_t<coot::f16>(kind, acc, partials, nparts, len, result, grid, ctx->stream); break;
     default: ce = coot::launch_combine_t<coot::s64>(kind, acc, partials, nparts, len, result, grid, ctx->stream); break;
   }
   if (ce != cudaSuccess) return cuda_fail(ce, "combine kernel launch");
@@ -1005,6 +1017,8 @@ coot_status coot_fill(coot_ctx* ctx, uint32_t elem, uint32_t fill_kind, uint64_t
     case COOT_F32: ce = coot::launch_fill_t<float>(fill_kind, seed, stream, start, count, n_rows, k, out, grid, ctx->stream); break;
     case COOT_F64: ce = coot::launch_fill_t<double>(fill_kind, seed, stream, start, count, n_rows, k, out, grid, ctx->stream); break;
     case COOT_U32: ce = coot::launch_fill_t<uint32_t>(fill_kind, seed, stream, start, count, n_rows, k, out, grid, ctx->stream); break;
+    case COOT_BF16: ce = coot::launch_fill_t<coot::bf16>(fill_kind, seed, stream, start, count, n_rows, k, out, grid, ctx->stream); break;
+    case COOT_F16: ce = coot::launch_fill_t<coot::f16>(fill_kind, seed, stream, start, count, n_rows, k, out, grid, ctx->stream); break;
     default: ce = coot::launch_fill_t<coot::s64>(fill_kind, seed, stream, start, count, n_rows, k, out, grid, ctx->stream); break;
   }
   if (ce != cudaSuccess) return cuda_fail(ce, "fill kernel launch");

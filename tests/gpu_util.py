@@ -5,7 +5,8 @@ import numpy as np
 import pytest
 import torch
 
-TORCH = {"f32": torch.float32, "f64": torch.float64, "u32": torch.uint32, "s64": torch.int64}
+TORCH = {"f32": torch.float32, "f64": torch.float64, "u32": torch.uint32, "s64": torch.int64,
+         "bf16": torch.bfloat16, "f16": torch.float16}
 
 
 def have_gpu() -> bool:
@@ -21,6 +22,8 @@ def to_dev(a: np.ndarray, etype: str, offset: int = 0) -> torch.Tensor:
     a = np.ascontiguousarray(a, dtype=_np_view(etype))
     if etype == "u32":
         t = torch.from_numpy(a.view(np.int32).copy()).view(torch.uint32)
+    elif etype == "bf16":  # host arrays hold bf16 bit patterns (uint16)
+        t = torch.from_numpy(a.view(np.int16).copy()).view(torch.bfloat16)
     else:
         t = torch.from_numpy(a.copy())
     base = torch.empty(a.size + offset + 8, dtype=TORCH[etype], device="cuda")
@@ -30,7 +33,8 @@ def to_dev(a: np.ndarray, etype: str, offset: int = 0) -> torch.Tensor:
 
 
 def _np_view(etype):
-    return {"f32": np.float32, "f64": np.float64, "u32": np.uint32, "s64": np.int64}[etype]
+    return {"f32": np.float32, "f64": np.float64, "u32": np.uint32, "s64": np.int64,
+            "bf16": np.uint16, "f16": np.float16}[etype]
 
 
 def empty_dev(n: int, etype: str, offset: int = 0) -> torch.Tensor:
@@ -41,4 +45,19 @@ def empty_dev(n: int, etype: str, offset: int = 0) -> torch.Tensor:
 def to_host(t: torch.Tensor, etype: str) -> np.ndarray:
     if etype == "u32":
         return t.cpu().view(torch.int32).numpy().view(np.uint32)
+    if etype == "bf16":
+        return t.cpu().view(torch.int16).numpy().view(np.uint16)
     return t.cpu().numpy()
+
+
+def half_ordinal(bits: np.ndarray) -> np.ndarray:
+    b = np.asarray(bits).view(np.uint16).astype(np.int64)
+    return np.where(b & 0x8000, -(b & 0x7FFF), b)
+
+
+def half_ulp(a, b) -> np.ndarray:
+    """Ordinal distance of 16-bit float bit patterns (NaN vs NaN -> 0)."""
+    a = np.atleast_1d(np.asarray(a)).view(np.uint16)
+    b = np.atleast_1d(np.asarray(b)).view(np.uint16)
+    d = np.abs(half_ordinal(a) - half_ordinal(b))
+    return d
