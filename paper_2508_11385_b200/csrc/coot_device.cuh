@@ -297,8 +297,39 @@ __device__ __forceinline__ double un(double a) {
   else if constexpr (OP == COOT_OP_LOG) return log(a);
   else return a;
 }
-// bf16 / f16 (R24): widen exactly, compute (f32 for + - * / sqrt, f64 for exp /
-// log), round once to the format.
+// bf16 / f16 EXP / LOG (R24): the f32 expf / logf result (CUDA math library:
+// <= 2 / <= 1 ulp) already decides the correctly rounded 16-bit value unless
+// it lies within a few f32 ulps of a rounding midpoint of the format (the
+// bits below the format's last place are 100...0 +- margin), or outside the
+// format's normal range, or is not finite.  Those rare elements (~2^-12 of
+// bf16, ~2^-9 of f16 results) take the f64 path, so every element still gets
+// the correctly rounded result while the common case stays in FP32/MUFU.
+//
+// half_mid_dist(y) = (bits below the last place - midpoint + margin) mod 2^b:
+// the rounding is undecided iff it is <= 2 * margin.  bf16 shares f32's
+// exponent range, so the last place is bit 16 for every f32 (subnormal
+// included) and inf / 0 / NaN round the same from y as from the true value
+// (an f32 result beyond FLT_MAX is far past bf16's overflow midpoint).  f16's
+// last place is bit 13 only in its normal range; results below 2^-14 go to
+// the fallback, results past 65520 round to inf either way.
+constexpr unsigned kHalfMargin = 8;  // f32 ulps (4x the library's bound)
+template <class H>
+__device__ __forceinline__ unsigned half_mid_dist(float y) {
+  const unsigned u = __float_as_uint(y);
+  if constexpr (std::is_same<H, bf16>::value) {
+    return (u + (0x8000u + kHalfMargin)) & 0xffffu;
+  } else {
+    const unsigned d = (u + (0x1000u + kHalfMargin)) & 0x1fffu;
+    return fabsf(y) < 0x1p-14f ? 0u : d;
+  }
+}
+template <class H>
+__device__ __forceinline__ bool half_round_decided(float y) {
+  return half_mid_dist<H>(y) > 2 * kHalfMargin;
+}
+
+// bf16 / f16 (R24): widen exactly, compute (f32 for + - * / sqrt, f32 with an
+// f64 fallback for exp / log), round once to the format.
 template <int OP, class H>
 __device__ __forceinline__ H half_un(H a) {
   if constexpr (OP == COOT_OP_NEG) return H((unsigned short)(a.bits ^ 0x8000u), true);
@@ -307,9 +338,15 @@ __device__ __forceinline__ H half_un(H a) {
     const float x = to_f32(a);
     if constexpr (OP == COOT_OP_SQUARE) return half_from_f32<H>(__fmul_rn(x, x));
     else if constexpr (OP == COOT_OP_SQRT) return half_from_f32<H>(__fsqrt_rn(x));
-    else if constexpr (OP == COOT_OP_EXP) return half_from_f64<H>(exp_f64_of_f32(x));
-    else if constexpr (OP == COOT_OP_LOG) return half_from_f64<H>(log((double)x));
-    else return a;
+    else if constexpr (OP == COOT_OP_EXP) {
+      const float y = expf(x);
+      if (__builtin_expect(half_round_decided<H>(y), 1)) return half_from_f32<H>(y);
+      return half_from_f64<H>(exp_f64_of_f32(x));
+    } else if constexpr (OP == COOT_OP_LOG) {
+      const float y = logf(x);
+      if (__builtin_expect(half_round_decided<H>(y), 1)) return half_from_f32<H>(y);
+      return half_from_f64<H>(log((double)x));
+    } else return a;
   }
 }
 template <int OP>
@@ -320,6 +357,11 @@ template <int OP>
 __device__ __forceinline__ f16 un(f16 a) {
   return half_un<OP, f16>(a);
 }
+// A unary node over the W elements one dispatch holds.  For bf16/f16 EXP/LOG
+// the fast f32 results of all W elements are formed first and the rare f64
+// fix-up runs after them under one branch, so the W dependency chains stay
+// independent (interleavable) instead of being split by a branch per element.
+// (defined after every un<> overload below)
 template <int OP, class H>
 __device__ __forceinline__ H half_bin(H a, H b) {
   const float x = to_f32(a), y = to_f32(b);
@@ -392,6 +434,32 @@ __device__ __forceinline__ s64 bin(s64 a, s64 b) {
   else if constexpr (OP == COOT_OP_MIN) return (b < a) ? b : a;
   else if constexpr (OP == COOT_OP_MAX) return (a < b) ? b : a;
   else return a;
+}
+
+template <int OP, class T, int W>
+__device__ __forceinline__ void un_vec(T (&v)[W]) {
+  if constexpr (is_half<T>() && (OP == COOT_OP_EXP || OP == COOT_OP_LOG)) {
+    float x[W];
+    unsigned closest = 0xffffffffu;
+#pragma unroll
+    for (int w = 0; w < W; ++w) {
+      x[w] = to_f32(v[w]);
+      const float y = (OP == COOT_OP_EXP) ? expf(x[w]) : logf(x[w]);
+      closest = min(closest, half_mid_dist<T>(y));
+      v[w] = half_from_f32<T>(y);
+    }
+    if (__builtin_expect(closest <= 2 * kHalfMargin, 0)) {
+#pragma unroll
+      for (int w = 0; w < W; ++w) {
+        const float y = (OP == COOT_OP_EXP) ? expf(x[w]) : logf(x[w]);
+        if (!half_round_decided<T>(y))
+          v[w] = half_from_f64<T>((OP == COOT_OP_EXP) ? exp_f64_of_f32(x[w]) : log((double)x[w]));
+      }
+    }
+  } else {
+#pragma unroll
+    for (int w = 0; w < W; ++w) v[w] = un<OP>(v[w]);
+  }
 }
 
 // ---- 16-byte streaming memory access --------------------------------------

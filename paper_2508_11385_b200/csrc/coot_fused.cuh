@@ -104,8 +104,7 @@ struct StaticStep {
 #pragma unroll
       for (int w = 0; w < W; ++w) st[SP][w] = s;
     } else if constexpr (is_unary_op(op)) {
-#pragma unroll
-      for (int w = 0; w < W; ++w) st[SP - 1][w] = un<op>(st[SP - 1][w]);
+      un_vec<op>(st[SP - 1]);
     } else {
 #pragma unroll
       for (int w = 0; w < W; ++w) st[SP - 2][w] = bin<op>(st[SP - 2][w], st[SP - 1][w]);
@@ -166,8 +165,7 @@ struct InterpEval {
 #define COOT_UN_CASE(OP, d)                                                \
   case COOT_KEY(COOT_OP_##OP, d):                                          \
     if constexpr ((d) >= 1 && (d) <= SMAX && op_legal<T>(COOT_OP_##OP)) {  \
-      _Pragma("unroll") for (int w = 0; w < W; ++w)                        \
-          st[(d) - 1][w] = un<COOT_OP_##OP>(st[(d) - 1][w]);                \
+      un_vec<COOT_OP_##OP>(st[(d) >= 1 ? (d) - 1 : 0]);                    \
     }                                                                      \
     break;
 #define COOT_BIN_CASE(OP, d)                                               \

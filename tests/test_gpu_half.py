@@ -80,6 +80,41 @@ def test_catalog_programs_bit_exact(ctxs, etype, cat):
 
 
 @pytest.mark.parametrize("etype", HALF)
+@pytest.mark.parametrize("op", ["EXP", "LOG", "SQRT", "SQUARE"])
+def test_unary_exhaustive(ctxs, etype, op):
+    """Every one of the 65536 bit patterns through each rounding unary op: covers
+    the f32 fast path and the f64 fallback near rounding midpoints (R24)."""
+    pats = np.arange(1 << 16, dtype=np.uint16)
+    x = pats if etype == "bf16" else pats.view(np.float16)
+    prog = P(f"L0 {op}")
+    want = oracle.eval_program(etype, prog, [x])
+    for name, ctx in ctxs.items():
+        got = run(ctx, etype, prog, [x], [])
+        nan_w = np.isnan(oracle.to_float(etype, want))
+        assert np.array_equal(nan_w, np.isnan(oracle.to_float(etype, got))), name
+        assert np.array_equal(bits(got)[~nan_w], bits(want)[~nan_w]), (
+            name, int(np.nonzero(bits(got)[~nan_w] != bits(want)[~nan_w])[0][0]))
+
+
+@pytest.mark.parametrize("etype", HALF)
+@pytest.mark.parametrize("op", ["ADD", "MUL", "DIV"])
+def test_binary_dense_sample(ctxs, etype, op):
+    """One operand exhaustive (all finite patterns), the other a fixed spread of
+    magnitudes: subnormal, overflow and tie cases of the single rounding."""
+    pats = np.arange(1 << 16, dtype=np.uint16)
+    a = pats if etype == "bf16" else pats.view(np.float16)
+    for bval in (3.0, -0.375, 1.0 / 3.0, 1e-3, 300.0):
+        b = np.full(a.size, oracle.half_from_double(etype, bval), dtype=np.uint16)
+        b = b if etype == "bf16" else b.view(np.float16)
+        prog = P(f"L0 L1 {op}")
+        want = oracle.eval_program(etype, prog, [a, b])
+        got = run(ctxs["tma"], etype, prog, [a, b], [])
+        nan_w = np.isnan(oracle.to_float(etype, want))
+        assert np.array_equal(nan_w, np.isnan(oracle.to_float(etype, got)))
+        assert np.array_equal(bits(got)[~nan_w], bits(want)[~nan_w]), (op, bval)
+
+
+@pytest.mark.parametrize("etype", HALF)
 def test_random_programs_bit_exact(ctxs, etype):
     rng = random.Random(77 + len(etype))
     for trial in range(25):

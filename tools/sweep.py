@@ -46,6 +46,14 @@ WL = {
     "imin_2p30": ("f32", 1 << 30, 1, "L0", [], "INDEX_MIN", False, False),
     "diag_add_1e4": ("f32", 10_000, 1, "L0 S0 ADD", [100.0], None, "diag", False),
     "submat_axpy": ("f32", 8192, 8192, "S0 L0 MUL L1 ADD", [2.5], "ACCU", "submat", False),
+    "bf16_c2_2p31": ("bf16", 1 << 31, 1, "L0 L1 MUL EXP S0 L2 MUL ADD", [3.0], "ACCU", False, False),
+    "bf16_c2_eval_2p30": ("bf16", 1 << 30, 1, "L0 L1 MUL EXP S0 L2 MUL ADD", [3.0], "ACCU", True, False),
+    "bf16_dot_2p31": ("bf16", 1 << 31, 1, "L0 L1 MUL", [], "ACCU", False, False),
+    "f16_c2_2p31": ("f16", 1 << 31, 1, "L0 L1 MUL EXP S0 L2 MUL ADD", [3.0], "ACCU", False, False),
+    "f16_axpy_eval_2p30": ("f16", 1 << 30, 1, "S0 L0 MUL L1 ADD", [2.5], None, True, False),
+    "bf16_var_2p31": ("bf16", 1 << 31, 1, "L0", [], "VAR", False, False),
+    "bf16_dim0": ("bf16", 32768, 32768, "L0", [], "SUM_DIM0", False, False),
+    "bf16_interp_c2": ("bf16", 1 << 30, 1, "L0 L1 MUL EXP S0 L2 MUL ADD", [3.0], "ACCU", True, True),
 }
 
 
