@@ -37,7 +37,11 @@
 /* ---- element types and opcodes (the oracle's own numbering) ------------ */
 /* BF16 / F16 (reading R24): 16-bit storage, every node rounded to the storage
  * format; the roadmap's low-precision types. */
-enum { ORC_F32 = 0, ORC_F64 = 1, ORC_U32 = 2, ORC_S64 = 3, ORC_BF16 = 4, ORC_F16 = 5 };
+/* E4M3 / E5M2 (reading R25): 8-bit STORAGE types — the expression is evaluated
+ * in f32 (every node an f32 node) and each element's value is rounded once to
+ * the 8-bit format; reductions consume those 8-bit values and return f32. */
+enum { ORC_F32 = 0, ORC_F64 = 1, ORC_U32 = 2, ORC_S64 = 3, ORC_BF16 = 4, ORC_F16 = 5,
+       ORC_E4M3 = 6, ORC_E5M2 = 7 };
 
 enum {
   ORC_LOAD = 0, ORC_SCALAR = 1,
@@ -60,13 +64,16 @@ static size_t esize(int type) {
     case ORC_S64: return 8;
     case ORC_BF16: return 2;
     case ORC_F16: return 2;
+    case ORC_E4M3: return 1;
+    case ORC_E5M2: return 1;
   }
   return 0;
 }
 
 static int is_half(int type) { return type == ORC_BF16 || type == ORC_F16; }
+static int is_fp8(int type) { return type == ORC_E4M3 || type == ORC_E5M2; }
 static int is_flt(int type) {
-  return type == ORC_F32 || type == ORC_F64 || is_half(type);
+  return type == ORC_F32 || type == ORC_F64 || is_half(type) || is_fp8(type);
 }
 
 /* ---- 16-bit float formats ------------------------------------------------
@@ -131,6 +138,69 @@ static uint16_t half_round(int type, __float128 x) {
 
 uint16_t orc_half_from_double(int type, double x) { return half_round(type, (__float128)x); }
 
+/* ---- 8-bit float formats (OCP 8-bit floating point) ------------------------
+ * E4M3 ("fn"): 1 sign, 4 exponent, 3 mantissa bits, bias 7, NO infinities:
+ *   exponent field 15 with mantissa 7 is NaN, so the largest finite is
+ *   1.75 * 2^8 = 448; subnormals m * 2^-9.
+ * E5M2: 1 sign, 5 exponent, 2 mantissa bits, bias 15, IEEE-style: field 31
+ *   is inf (m = 0) / NaN; largest finite 1.75 * 2^15 = 57344; subnormals
+ *   m * 2^-16.
+ * fp8_round: round-to-nearest-even of the exact value, SATURATING to the
+ * largest finite magnitude on overflow and for +-inf (reading R25: the
+ * hardware conversion to these formats is the saturating one); NaN -> 0x7f. */
+static void fmt8_of(int type, int* ebits, int* mbits) {
+  *ebits = type == ORC_E4M3 ? 4 : 5;
+  *mbits = type == ORC_E4M3 ? 3 : 2;
+}
+
+static double fp8_decode(int type, uint8_t b) {
+  int ebits, mbits;
+  fmt8_of(type, &ebits, &mbits);
+  const int bias = (1 << (ebits - 1)) - 1;
+  const int sign = b >> 7;
+  const int e = (b >> mbits) & ((1 << ebits) - 1);
+  const int m = b & ((1 << mbits) - 1);
+  double v;
+  if (type == ORC_E4M3 && e == 15 && m == 7) v = NAN;
+  else if (type == ORC_E5M2 && e == 31) v = m ? NAN : INFINITY;
+  else if (e == 0) v = ldexp((double)m, 1 - bias - mbits);
+  else v = ldexp((double)(m | (1 << mbits)), e - bias - mbits);
+  return sign ? -v : v;
+}
+
+static uint8_t fp8_round(int type, __float128 x) {
+  int ebits, mbits;
+  fmt8_of(type, &ebits, &mbits);
+  const int bias = (1 << (ebits - 1)) - 1;
+  /* largest finite: E4M3 0x7e (field 15, m 6), E5M2 0x7b (field 30, m 3) */
+  const uint8_t maxfin = type == ORC_E4M3 ? 0x7e : 0x7b;
+  if (isnanq(x)) return 0x7f;
+  const uint8_t sign = signbitq(x) ? 0x80 : 0;
+  __float128 a = fabsq(x);
+  if (isinfq(a)) return (uint8_t)(sign | maxfin);
+  if (a == 0) return sign;
+  int k;
+  frexpq(a, &k);
+  const int E = k - 1;                            /* 2^E <= a < 2^(E+1) */
+  const int emin = 1 - bias;
+  const int qe = (E < emin ? emin : E) - mbits;   /* exponent of one ulp */
+  const __float128 scaled = ldexpq(a, -qe);
+  uint64_t n = (uint64_t)floorq(scaled);
+  const __float128 rem = scaled - (__float128)n;
+  if (rem > 0.5Q || (rem == 0.5Q && (n & 1))) ++n;
+  if (n < (1ull << mbits)) return (uint8_t)(sign | n);   /* subnormal */
+  int eq = qe;
+  if (n == (2ull << mbits)) { n >>= 1; ++eq; }
+  const int field = eq + mbits + bias;
+  const uint8_t code = (uint8_t)((field << mbits) | (int)(n - (1ull << mbits)));
+  /* beyond the largest finite (incl. E4M3's NaN slot / E5M2's inf field) */
+  if (field > (1 << ebits) - 1 || code > maxfin) return (uint8_t)(sign | maxfin);
+  return (uint8_t)(sign | code);
+}
+
+uint8_t orc_fp8_from_double(int type, double x) { return fp8_round(type, (__float128)x); }
+double orc_fp8_to_double(int type, uint8_t b) { return fp8_decode(type, b); }
+
 /* ---- input generator ----------------------------------------------------
  * mix(z): SplitMix64 finaliser (Vigna, splitmix64.c).
  * key = seed ^ (stream * 0xD1B54A32D192ED03)
@@ -174,6 +244,8 @@ static void fill_one(int type, int kind, uint64_t seed, uint64_t stream,
       /* uniform [0,1) on the format's significand grid (exactly representable) */
       case ORC_BF16: ((uint16_t*)out)[idx] = half_round(type, (__float128)(h >> 56) * 0x1p-8Q); break;
       case ORC_F16: ((uint16_t*)out)[idx] = half_round(type, (__float128)(h >> 53) * 0x1p-11Q); break;
+      case ORC_E4M3: ((uint8_t*)out)[idx] = fp8_round(type, (__float128)(h >> 60) * 0x1p-4Q); break;
+      case ORC_E5M2: ((uint8_t*)out)[idx] = fp8_round(type, (__float128)(h >> 61) * 0x1p-3Q); break;
     }
   } else {
     switch (type) {
@@ -183,6 +255,8 @@ static void fill_one(int type, int kind, uint64_t seed, uint64_t stream,
       case ORC_S64: ((int64_t*)out)[idx] = (int64_t)iv; break;
       case ORC_BF16:
       case ORC_F16: ((uint16_t*)out)[idx] = half_round(type, (__float128)iv); break;
+      case ORC_E4M3:
+      case ORC_E5M2: ((uint8_t*)out)[idx] = fp8_round(type, (__float128)iv); break;
     }
   }
 }
@@ -385,9 +459,44 @@ static void apply_binary(int type, int op, uint64_t n, const void* a, const void
 
 int orc_eval(int type, uint64_t n, const void* const* operands, int n_operands,
              const void* scalars, int n_scalars, const int* ops, const int* args,
+             int n_instr, void* out);
+
+/* 8-bit storage types (reading R25): decode every operand exactly to f32,
+ * evaluate the program as an f32 program (scalars are f32), round each
+ * element's final value once to the 8-bit format. */
+static int eval_fp8(int type, uint64_t n, const void* const* operands, int n_operands,
+                    const void* scalars, int n_scalars, const int* ops, const int* args,
+                    int n_instr, void* out) {
+  if (n_operands < 0 || n_operands > ORC_MAX_STACK) return ORC_E_PROGRAM;
+  size_t fb = (size_t)(n ? n : 1) * sizeof(float);
+  float* dec[ORC_MAX_STACK];
+  const void* cdec[ORC_MAX_STACK];
+  float* res = (float*)malloc(fb);
+  int rc = res ? ORC_E_OK : ORC_E_NOMEM;
+  int made = 0;
+  for (; rc == ORC_E_OK && made < n_operands; ++made) {
+    dec[made] = (float*)malloc(fb);
+    if (!dec[made]) { rc = ORC_E_NOMEM; break; }
+    for (uint64_t i = 0; i < n; ++i)
+      dec[made][i] = (float)fp8_decode(type, ((const uint8_t*)operands[made])[i]);
+    cdec[made] = dec[made];
+  }
+  if (rc == ORC_E_OK)
+    rc = orc_eval(ORC_F32, n, cdec, n_operands, scalars, n_scalars, ops, args, n_instr, res);
+  if (rc == ORC_E_OK)
+    for (uint64_t i = 0; i < n; ++i) ((uint8_t*)out)[i] = fp8_round(type, (__float128)res[i]);
+  for (int k = 0; k < made; ++k) free(dec[k]);
+  free(res);
+  return rc;
+}
+
+int orc_eval(int type, uint64_t n, const void* const* operands, int n_operands,
+             const void* scalars, int n_scalars, const int* ops, const int* args,
              int n_instr, void* out) {
   size_t es = esize(type);
   if (es == 0) return ORC_E_TYPE;
+  if (is_fp8(type))
+    return eval_fp8(type, n, operands, n_operands, scalars, n_scalars, ops, args, n_instr, out);
   void* stack[ORC_MAX_STACK];
   int sp = 0;
   int rc = ORC_E_OK;

@@ -436,23 +436,60 @@ __device__ __forceinline__ s64 bin(s64 a, s64 b) {
   else return a;
 }
 
+// Round W f32 values to a 16-bit format two at a time: cvt.rn.{bf16x2,f16x2}.f32
+// (F2FP.PACK_AB, one instruction per pair, not on the quarter-rate XU pipe that
+// the single-value F2F conversion occupies).  Same RNE result per element.
+template <class H, int W>
+__device__ __forceinline__ void half_round_vec(const float (&y)[W], H (&v)[W]) {
+#pragma unroll
+  for (int w = 0; w + 1 < W; w += 2) {
+    unsigned p;
+    if constexpr (std::is_same<H, bf16>::value) {
+      asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(p) : "f"(y[w + 1]), "f"(y[w]));
+    } else {
+      asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(p) : "f"(y[w + 1]), "f"(y[w]));
+    }
+    v[w] = H((unsigned short)(p & 0xffffu), true);
+    v[w + 1] = H((unsigned short)(p >> 16), true);
+  }
+  if constexpr (W & 1) v[W - 1] = half_from_f32<H>(y[W - 1]);
+}
+
+template <int OP, class T, int W>
+__device__ __forceinline__ void bin_vec(T (&a)[W], const T (&b)[W]) {
+  if constexpr (is_half<T>() && (OP == COOT_OP_ADD || OP == COOT_OP_SUB || OP == COOT_OP_MUL ||
+                                 OP == COOT_OP_DIV)) {
+    float y[W];
+#pragma unroll
+    for (int w = 0; w < W; ++w) y[w] = bin<OP>(to_f32(a[w]), to_f32(b[w]));
+    half_round_vec<T, W>(y, a);
+  } else {
+#pragma unroll
+    for (int w = 0; w < W; ++w) a[w] = bin<OP>(a[w], b[w]);
+  }
+}
+
 template <int OP, class T, int W>
 __device__ __forceinline__ void un_vec(T (&v)[W]) {
-  if constexpr (is_half<T>() && (OP == COOT_OP_EXP || OP == COOT_OP_LOG)) {
-    float x[W];
+  if constexpr (is_half<T>() && (OP == COOT_OP_SQUARE || OP == COOT_OP_SQRT)) {
+    float y[W];
+#pragma unroll
+    for (int w = 0; w < W; ++w) y[w] = un<OP>(to_f32(v[w]));
+    half_round_vec<T, W>(y, v);
+  } else if constexpr (is_half<T>() && (OP == COOT_OP_EXP || OP == COOT_OP_LOG)) {
+    float x[W], y[W];
     unsigned closest = 0xffffffffu;
 #pragma unroll
     for (int w = 0; w < W; ++w) {
       x[w] = to_f32(v[w]);
-      const float y = (OP == COOT_OP_EXP) ? expf(x[w]) : logf(x[w]);
-      closest = min(closest, half_mid_dist<T>(y));
-      v[w] = half_from_f32<T>(y);
+      y[w] = (OP == COOT_OP_EXP) ? expf(x[w]) : logf(x[w]);
+      closest = min(closest, half_mid_dist<T>(y[w]));
     }
+    half_round_vec<T, W>(y, v);
     if (__builtin_expect(closest <= 2 * kHalfMargin, 0)) {
 #pragma unroll
       for (int w = 0; w < W; ++w) {
-        const float y = (OP == COOT_OP_EXP) ? expf(x[w]) : logf(x[w]);
-        if (!half_round_decided<T>(y))
+        if (!half_round_decided<T>(y[w]))
           v[w] = half_from_f64<T>((OP == COOT_OP_EXP) ? exp_f64_of_f32(x[w]) : log((double)x[w]));
       }
     }

@@ -106,8 +106,7 @@ struct StaticStep {
     } else if constexpr (is_unary_op(op)) {
       un_vec<op>(st[SP - 1]);
     } else {
-#pragma unroll
-      for (int w = 0; w < W; ++w) st[SP - 2][w] = bin<op>(st[SP - 2][w], st[SP - 1][w]);
+      bin_vec<op>(st[SP - 2], st[SP - 1]);
     }
     if constexpr (sizeof...(Rest) > 0) StaticStep<T, W, nsp, Rest...>::run(st, src, a);
   }
@@ -171,8 +170,7 @@ struct InterpEval {
 #define COOT_BIN_CASE(OP, d)                                               \
   case COOT_KEY(COOT_OP_##OP, d):                                          \
     if constexpr ((d) >= 2 && (d) <= SMAX && op_legal<T>(COOT_OP_##OP)) {  \
-      _Pragma("unroll") for (int w = 0; w < W; ++w)                        \
-          st[(d) - 2][w] = bin<COOT_OP_##OP>(st[(d) - 2][w], st[(d) - 1][w]); \
+      bin_vec<COOT_OP_##OP>(st[(d) >= 2 ? (d) - 2 : 0], st[(d) >= 2 ? (d) - 1 : 0]); \
     }                                                                      \
     break;
 #define COOT_D(M, ...) M(__VA_ARGS__ 0) M(__VA_ARGS__ 1) M(__VA_ARGS__ 2) M(__VA_ARGS__ 3) \
