@@ -21,10 +21,13 @@ import numpy as np
 
 from . import build as _build
 
-TYPES = {"f32": 0, "f64": 1, "u32": 2, "s64": 3, "bf16": 4, "f16": 5}
-# bf16 arrays are carried as their uint16 bit patterns (numpy has no bfloat16)
+TYPES = {"f32": 0, "f64": 1, "u32": 2, "s64": 3, "bf16": 4, "f16": 5, "e4m3": 6, "e5m2": 7}
+# bf16 / fp8 arrays are carried as their bit patterns (numpy has no such dtypes)
 DTYPES = {"f32": np.float32, "f64": np.float64, "u32": np.uint32, "s64": np.int64,
-          "bf16": np.uint16, "f16": np.float16}
+          "bf16": np.uint16, "f16": np.float16, "e4m3": np.uint8, "e5m2": np.uint8}
+FP8 = ("e4m3", "e5m2")
+# reduction / dim-sum / statistics result dtype: eT, f32 for the fp8 storage types (R25)
+RDTYPES = dict(DTYPES, e4m3=np.float32, e5m2=np.float32)
 
 
 def bf16_to_f32(bits: np.ndarray) -> np.ndarray:
@@ -32,10 +35,17 @@ def bf16_to_f32(bits: np.ndarray) -> np.ndarray:
     return (np.asarray(bits, dtype=np.uint16).astype(np.uint32) << 16).view(np.float32)
 
 
+def fp8_table(etype: str) -> np.ndarray:
+    """The 256 exact values of an fp8 format, indexed by bit pattern."""
+    return np.array([lib().orc_fp8_to_double(TYPES[etype], b) for b in range(256)])
+
+
 def to_float(etype: str, a: np.ndarray) -> np.ndarray:
     """Exact float64 values of an array of any float element type."""
     if etype == "bf16":
         return bf16_to_f32(a).astype(np.float64)
+    if etype in FP8:
+        return fp8_table(etype)[np.asarray(a, dtype=np.uint8)]
     return np.asarray(a).astype(np.float64)
 OPS = {
     "LOAD": 0, "SCALAR": 1, "NEG": 2, "ABS": 3, "SQUARE": 4, "SQRT": 5, "EXP": 6,
@@ -55,6 +65,10 @@ def lib():
         u64, i32, vp = ctypes.c_uint64, ctypes.c_int, ctypes.c_void_p
         L.orc_half_from_double.restype = ctypes.c_uint16
         L.orc_half_from_double.argtypes = [i32, ctypes.c_double]
+        L.orc_fp8_from_double.restype = ctypes.c_uint8
+        L.orc_fp8_from_double.argtypes = [i32, ctypes.c_double]
+        L.orc_fp8_to_double.restype = ctypes.c_double
+        L.orc_fp8_to_double.argtypes = [i32, ctypes.c_uint8]
         L.orc_hash.restype = u64
         L.orc_hash.argtypes = [u64, u64, u64]
         L.orc_fill.restype = i32
@@ -120,12 +134,19 @@ def _scalar_array(etype: str, scalars):
     if etype in ("bf16", "f16"):  # R4: the scalar rounded once to the 16-bit format
         bits = [lib().orc_half_from_double(TYPES[etype], float(s)) for s in (scalars or [0])]
         return np.array(bits, dtype=np.uint16).view(DTYPES[etype])
+    if etype in FP8:  # R25: the arithmetic type is f32, so scalars are f32
+        return np.array(list(scalars) if scalars else [0], dtype=np.float32)
     return np.array(list(scalars) if scalars else [0], dtype=DTYPES[etype])
 
 
 def half_from_double(etype: str, x: float) -> int:
     """Bits of x rounded (nearest-even) to bf16 / f16."""
     return int(lib().orc_half_from_double(TYPES[etype], float(x)))
+
+
+def fp8_from_double(etype: str, x: float) -> int:
+    """Bits of x rounded (nearest-even, saturating) to e4m3 / e5m2."""
+    return int(lib().orc_fp8_from_double(TYPES[etype], float(x)))
 
 
 def eval_program(etype: str, program, operands, scalars=()) -> np.ndarray:
@@ -146,10 +167,11 @@ def eval_program(etype: str, program, operands, scalars=()) -> np.ndarray:
 
 
 def reduce(etype: str, kind: str, v: np.ndarray):
-    """Full reduction; returns a numpy scalar of eT, or a 2-array for MINMAX."""
+    """Full reduction; returns a numpy scalar of eT (f32 for fp8), or a 2-array
+    for MINMAX."""
     dt = DTYPES[etype]
     v = np.ascontiguousarray(v, dtype=dt)
-    out = np.zeros(2, dtype=dt)
+    out = np.zeros(2, dtype=RDTYPES[etype])
     _check(lib().orc_reduce(TYPES[etype], KINDS[kind], v.size, _ptr(v), _ptr(out)), "reduce")
     return out.copy() if kind == "MINMAX" else out[0]
 
@@ -164,7 +186,7 @@ def stats(etype: str, kind: str, v: np.ndarray):
     if kind.startswith("INDEX"):
         out = np.zeros(1, dtype=np.uint64)
     else:
-        out = np.zeros(1, dtype=dt)
+        out = np.zeros(1, dtype=RDTYPES[etype])
     _check(lib().orc_stats(TYPES[etype], STATS[kind], v.size, _ptr(v), _ptr(out)), "stats")
     return int(out[0]) if kind.startswith("INDEX") else out[0]
 
@@ -182,7 +204,7 @@ class Accumulator:
         _check(lib().orc_acc_add(self._buf, v.size, _ptr(v)), "acc_add")
 
     def final(self):
-        out = np.zeros(2, dtype=DTYPES[self.etype])
+        out = np.zeros(2, dtype=RDTYPES[self.etype])
         _check(lib().orc_acc_final(self._buf, _ptr(out)), "acc_final")
         return out.copy() if self.kind == "MINMAX" else out[0]
 
@@ -193,7 +215,7 @@ def sum_dim(etype: str, dim: int, X: np.ndarray, n_rows: int, n_cols: int) -> np
     X = np.ascontiguousarray(X, dtype=dt).reshape(-1)
     if X.size != n_rows * n_cols:
         raise ValueError("X size mismatch")
-    out = np.empty(n_cols if dim == 0 else n_rows, dtype=dt)
+    out = np.empty(n_cols if dim == 0 else n_rows, dtype=RDTYPES[etype])
     _check(lib().orc_sum_dim(TYPES[etype], dim, n_rows, n_cols, _ptr(X), _ptr(out)), "sum_dim")
     return out
 

@@ -469,8 +469,8 @@ static int eval_fp8(int type, uint64_t n, const void* const* operands, int n_ope
                     int n_instr, void* out) {
   if (n_operands < 0 || n_operands > ORC_MAX_STACK) return ORC_E_PROGRAM;
   size_t fb = (size_t)(n ? n : 1) * sizeof(float);
-  float* dec[ORC_MAX_STACK];
-  const void* cdec[ORC_MAX_STACK];
+  float* dec[ORC_MAX_STACK] = {0};
+  const void* cdec[ORC_MAX_STACK] = {0};
   float* res = (float*)malloc(fb);
   int rc = res ? ORC_E_OK : ORC_E_NOMEM;
   int made = 0;
@@ -586,13 +586,20 @@ static void neumaier(long double* s, long double* c, long double x) {
 static long double elem_as_ld(int type, const void* v, uint64_t i) {
   if (type == ORC_F32) return (long double)((const float*)v)[i];
   if (is_half(type)) return (long double)half_decode(type, ((const uint16_t*)v)[i]);
+  if (is_fp8(type)) return (long double)fp8_decode(type, ((const uint8_t*)v)[i]);
   return (long double)((const double*)v)[i];
 }
 
-/* Round an exact-ish binary128 value once to the float type and store it. */
+/* Size of one reduction result: eT, except f32 for the 8-bit storage types
+ * (R25: their sums, norms and statistics are returned in f32). */
+static size_t rsize(int type) { return is_fp8(type) ? 4 : esize(type); }
+
+/* Round an exact-ish binary128 value once to the result type and store it. */
 static void store_flt(int type, void* out, size_t idx, __float128 r) {
   switch (type) {
-    case ORC_F32: ((float*)out)[idx] = (float)r; break;
+    case ORC_F32:
+    case ORC_E4M3:
+    case ORC_E5M2: ((float*)out)[idx] = (float)r; break;
     case ORC_F64: ((double*)out)[idx] = (double)r; break;
     default: ((uint16_t*)out)[idx] = half_round(type, r); break;
   }
@@ -727,7 +734,9 @@ int orc_stats(int type, int kind, uint64_t n, const void* v, void* result) {
           break;
         }
         case ORC_BF16:
-        case ORC_F16: {
+        case ORC_F16:
+        case ORC_E4M3:
+        case ORC_E5M2: {
           double a = (double)elem_as_ld(type, v, i), b = (double)elem_as_ld(type, v, best);
           better = kind == ORC_IMIN ? (a < b) : (a > b);
           break;
@@ -783,7 +792,7 @@ int orc_sum_dim(int type, int dim, uint64_t m, uint64_t n, const void* X, void* 
       orc_acc a;
       orc_acc_init(&a, type, ORC_ACCU);
       orc_acc_add(&a, m, (const char*)X + (size_t)(j * m) * es);
-      orc_acc_final(&a, (char*)out + (size_t)j * es);
+      orc_acc_final(&a, (char*)out + (size_t)j * rsize(type));
     }
     return ORC_E_OK;
   }
@@ -813,8 +822,7 @@ int orc_sum_dim(int type, int dim, uint64_t m, uint64_t n, const void* X, void* 
       case ORC_F64: ((double*)out)[i] = (double)((__float128)s[i] + (__float128)c[i]); break;
       case ORC_U32: ((uint32_t*)out)[i] = (uint32_t)u[i]; break;
       case ORC_S64: ((uint64_t*)out)[i] = u[i]; break;
-      case ORC_BF16:
-      case ORC_F16: store_flt(type, out, i, (__float128)s[i] + (__float128)c[i]); break;
+      default: store_flt(type, out, i, (__float128)s[i] + (__float128)c[i]); break;
     }
   }
   free(s);
