@@ -210,6 +210,10 @@ __device__ __forceinline__ double as_double(bf16 v) { return (double)to_f32(v); 
 __device__ __forceinline__ double as_double(f16 v) { return (double)to_f32(v); }
 __device__ __forceinline__ double as_double(uint32_t v) { return (double)v; }
 __device__ __forceinline__ double as_double(s64 v) { return (double)v; }
+// exact value of an f32 / 16-bit element as f32
+__device__ __forceinline__ float as_float(float v) { return v; }
+__device__ __forceinline__ float as_float(bf16 v) { return to_f32(v); }
+__device__ __forceinline__ float as_float(f16 v) { return to_f32(v); }
 // ordering (IEEE semantics for floats)
 template <class T>
 __device__ __forceinline__ bool lt(T a, T b) {
@@ -761,15 +765,31 @@ struct Accum {
   __device__ __forceinline__ void add(const T (&v)[W]) {
     if constexpr (ACC == ACC_VAR) {
       if (n == 0) c = as_double(v[0]);  // the shift: the thread's first element
-      double a1 = 0.0, a2 = 0.0;     // the unit's shifted sums, then one update each
+      if constexpr (std::is_same<T, double>::value || !is_float<T>()) {
+        double a1 = 0.0, a2 = 0.0;  // the unit's shifted sums, then one update each
 #pragma unroll
-      for (int w = 0; w < W; ++w) {
-        const double d = __dsub_rn(as_double(v[w]), c);
-        a1 = __dadd_rn(a1, d);
-        a2 = __fma_rn(d, d, a2);
+        for (int w = 0; w < W; ++w) {
+          const double d = __dsub_rn(as_double(v[w]), c);
+          a1 = __dadd_rn(a1, d);
+          a2 = __fma_rn(d, d, a2);
+        }
+        s1 = __dadd_rn(s1, a1);
+        s2 = __dadd_rn(s2, a2);
+      } else {
+        // f32 / 16-bit: the unit's shifted sums in f32 (the shift is an element,
+        // so exact in f32; x - c is exact when x is near c), widened to f64 once
+        // per unit — relative error ~W * 2^-24, far inside the 1e-5 bar
+        const float cf = (float)c;
+        float a1 = 0.f, a2 = 0.f;
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+          const float d = __fsub_rn(as_float(v[w]), cf);
+          a1 = __fadd_rn(a1, d);
+          a2 = __fmaf_rn(d, d, a2);
+        }
+        s1 = __dadd_rn(s1, (double)a1);
+        s2 = __dadd_rn(s2, (double)a2);
       }
-      s1 = __dadd_rn(s1, a1);
-      s2 = __dadd_rn(s2, a2);
       n += W;
     } else if constexpr (ACC == ACC_SUM) {
       s = sum_add<S>(s, unit_sum<T, W>(v));
