@@ -55,9 +55,17 @@ extern "C" {
 
 /* BF16 / F16: 16-bit float storage (the roadmap's low precision, P:596-603;
  * R24): every node is computed exactly or in f32/f64 and rounded once to the
- * 16-bit format; reductions accumulate in f64 and round once. */
+ * 16-bit format; reductions accumulate in f64 and round once.
+ * E4M3 / E5M2: 8-bit float STORAGE types (OCP FP8, "fp8 storage" of the same
+ * roadmap item; R25): operands are decoded exactly to f32, the program runs
+ * as an f32 program (scalars are given in the .f32 slot), and each element's
+ * final value is rounded once to the 8-bit format (nearest-even, saturating
+ * to the largest finite magnitude; NaN stays NaN).  Reductions consume those
+ * 8-bit values and their RESULTS ARE f32 (float), as are SUM_DIM vectors and
+ * MEAN / VAR / STDDEV / NORM2 / MIN / MAX. */
 typedef enum {
-  COOT_F32 = 0, COOT_F64 = 1, COOT_U32 = 2, COOT_S64 = 3, COOT_BF16 = 4, COOT_F16 = 5
+  COOT_F32 = 0, COOT_F64 = 1, COOT_U32 = 2, COOT_S64 = 3, COOT_BF16 = 4, COOT_F16 = 5,
+  COOT_E4M3 = 6, COOT_E5M2 = 7
 } coot_elem_t;
 
 typedef enum {
@@ -94,7 +102,8 @@ typedef struct {
 } coot_instr;
 
 /* A scalar operand, stored AS the element type (R4): the value 2.5 of an f32
- * expression is {.f32 = 2.5f}. */
+ * expression is {.f32 = 2.5f}; for E4M3 / E5M2 expressions it is stored as
+ * the arithmetic type f32 (R25). */
 typedef union {
   float f32;
   double f64;
@@ -136,18 +145,19 @@ typedef struct {
   coot_instr prog[COOT_MAX_INSTR];
 } coot_expr;
 
-/* Terminal reductions and the shape of `result`:
- *   ACCU, MIN, MAX, NORM2 -> 1 eT;  MINMAX -> 2 eT [min, max];
- *   SUM_DIM0 -> n_cols eT (a Row of column sums);
- *   SUM_DIM1 -> n_rows eT (a Col of row sums).
+/* Terminal reductions and the shape of `result` (rT = eT, except rT = f32
+ * for COOT_E4M3 / COOT_E5M2):
+ *   ACCU, MIN, MAX, NORM2 -> 1 rT;  MINMAX -> 2 rT [min, max];
+ *   SUM_DIM0 -> n_cols rT (a Row of column sums);
+ *   SUM_DIM1 -> n_rows rT (a Col of row sums).
  * ACCU of floats accumulates in f64 and rounds once to eT (R10); integer
  * ACCU is modular.  NORM2 = sqrt(sum v^2), floats only (R12).
  * MIN/MAX/MINMAX of an empty expression -> COOT_ERR_CONTRACT; ACCU, NORM2 of
  * empty -> 0; SUM_DIM over a zero-length dimension -> zeros.
- * Statistics ("mean, variance"; Armadillo semantics, R22), f32/f64 only:
- *   MEAN -> 1 eT = sum / n (empty -> COOT_ERR_CONTRACT);
- *   VAR  -> 1 eT = sum (v - mean)^2 / (n - 1)  (n == 1 -> 0; empty -> contract);
- *   STDDEV -> 1 eT = sqrt(VAR).  One pass: shifted sums per thread merged with
+ * Statistics ("mean, variance"; Armadillo semantics, R22), float types only:
+ *   MEAN -> 1 rT = sum / n (empty -> COOT_ERR_CONTRACT);
+ *   VAR  -> 1 rT = sum (v - mean)^2 / (n - 1)  (n == 1 -> 0; empty -> contract);
+ *   STDDEV -> 1 rT = sqrt(VAR).  One pass: shifted sums per thread merged with
  *   Chan's pairwise update in a fixed order (deterministic).
  * INDEX_MIN / INDEX_MAX -> 1 u64: the index (column-major linear) of the FIRST
  *   occurrence of the smallest / largest element (empty -> contract). */

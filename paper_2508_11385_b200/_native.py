@@ -20,7 +20,7 @@ MAX_INSTR = 32
 MAX_STACK = 8
 PARTIAL_BYTES = 32
 
-ELEM = {"f32": 0, "f64": 1, "u32": 2, "s64": 3, "bf16": 4, "f16": 5}
+ELEM = {"f32": 0, "f64": 1, "u32": 2, "s64": 3, "bf16": 4, "f16": 5, "e4m3": 6, "e5m2": 7}
 OP = {"LOAD": 0, "SCALAR": 1, "NEG": 2, "ABS": 3, "SQUARE": 4, "SQRT": 5, "EXP": 6, "LOG": 7,
       "ADD": 8, "SUB": 9, "MUL": 10, "DIV": 11, "MIN": 12, "MAX": 13}
 KIND = {"ACCU": 0, "MIN": 1, "MAX": 2, "MINMAX": 3, "NORM2": 4, "SUM_DIM0": 5, "SUM_DIM1": 6,
@@ -196,7 +196,8 @@ def half_bits(value: float, elem: str) -> int:
 
 def set_scalar(slot: Scalar, elem: str, value):
     """Store a scalar AS the element type (R4); reject lossy integer scalars."""
-    if elem == "f32":
+    if elem in ("f32", "e4m3", "e5m2"):  # 8-bit storage types compute in f32 (R25)
+        slot.bits = 0
         slot.f32 = float(value)
     elif elem == "f64":
         slot.f64 = float(value)

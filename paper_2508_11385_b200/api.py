@@ -24,9 +24,12 @@ from . import _native as N
 from ._native import CootError, check, lib
 
 TORCH_DTYPE = {"f32": torch.float32, "f64": torch.float64, "u32": torch.uint32,
-               "s64": torch.int64, "bf16": torch.bfloat16, "f16": torch.float16}
+               "s64": torch.int64, "bf16": torch.bfloat16, "f16": torch.float16,
+               "e4m3": torch.float8_e4m3fn, "e5m2": torch.float8_e5m2}
 ELEM_OF = {v: k for k, v in TORCH_DTYPE.items()}
-ESIZE = {"f32": 4, "f64": 8, "u32": 4, "s64": 8, "bf16": 2, "f16": 2}
+ESIZE = {"f32": 4, "f64": 8, "u32": 4, "s64": 8, "bf16": 2, "f16": 2, "e4m3": 1, "e5m2": 1}
+# reduction / dim-sum result dtype: eT, f32 for the 8-bit storage types (R25)
+RESULT_DTYPE = dict(TORCH_DTYPE, e4m3=torch.float32, e5m2=torch.float32)
 
 
 def elem_of(t: torch.Tensor) -> str:
@@ -496,7 +499,7 @@ def _reduce(e, kind, ctx=None, out: Mat | None = None):
     lw = lower(as_expr(e))
     ctx = ctx or default_ctx(lw.device_index())
     shape = {"MINMAX": (2,), "SUM_DIM0": (lw.n_cols,), "SUM_DIM1": (lw.n_rows,)}.get(kind, (1,))
-    dtype = torch.int64 if kind.startswith("INDEX") else TORCH_DTYPE[lw.elem]
+    dtype = torch.int64 if kind.startswith("INDEX") else RESULT_DTYPE[lw.elem]
     result = torch.empty(shape, dtype=dtype, device=lw.device())
     ctx.reduce(lw.elem, lw.n_rows, lw.n_cols, lw.program, lw.operands, lw.scalars, kind, result,
                out.data if out is not None else None)

@@ -40,6 +40,48 @@ struct f16 {
   __host__ __device__ constexpr explicit f16(int) : bits(0) {}
   __host__ __device__ constexpr f16(unsigned short b, bool) : bits(b) {}
 };
+// 8-bit float STORAGE types (R25, OCP E4M3 "fn" / E5M2): elements are decoded
+// exactly to f32, the program runs as an f32 program, and the element's final
+// value is rounded once (RNE, saturating: cvt.rn.satfinite) to the format.
+// Reductions consume those 8-bit values and return f32.
+struct e4m3 {
+  uint8_t bits;
+  __host__ __device__ constexpr e4m3() : bits(0) {}
+  __host__ __device__ constexpr explicit e4m3(int) : bits(0) {}
+  __host__ __device__ constexpr e4m3(unsigned char b, bool) : bits(b) {}
+};
+struct e5m2 {
+  uint8_t bits;
+  __host__ __device__ constexpr e5m2() : bits(0) {}
+  __host__ __device__ constexpr explicit e5m2(int) : bits(0) {}
+  __host__ __device__ constexpr e5m2(unsigned char b, bool) : bits(b) {}
+};
+// arithmetic type of an expression over T (f32 for the 8-bit storage types)
+template <class T>
+struct ComputeT {
+  typedef T type;
+};
+template <>
+struct ComputeT<e4m3> {
+  typedef float type;
+};
+template <>
+struct ComputeT<e5m2> {
+  typedef float type;
+};
+// type of a reduction / dim-sum result (eT; f32 for the 8-bit storage types)
+template <class T>
+struct ResultT {
+  typedef T type;
+};
+template <>
+struct ResultT<e4m3> {
+  typedef float type;
+};
+template <>
+struct ResultT<e5m2> {
+  typedef float type;
+};
 
 enum AccKind {
   ACC_NONE = 0, ACC_SUM = 1, ACC_SUMSQ = 2, ACC_MINMAX = 3,
@@ -118,6 +160,15 @@ template <>
 __device__ __forceinline__ f16 scalar_as<f16>(u64 bits) {
   return f16((unsigned short)bits, true);
 }
+// (8-bit types: only partial records carry their bits; program scalars are f32)
+template <>
+__device__ __forceinline__ e4m3 scalar_as<e4m3>(u64 bits) {
+  return e4m3((unsigned char)bits, true);
+}
+template <>
+__device__ __forceinline__ e5m2 scalar_as<e5m2>(u64 bits) {
+  return e5m2((unsigned char)bits, true);
+}
 
 template <class T>
 __device__ __forceinline__ u64 to_bits(T v);
@@ -143,6 +194,14 @@ __device__ __forceinline__ u64 to_bits<bf16>(bf16 v) {
 }
 template <>
 __device__ __forceinline__ u64 to_bits<f16>(f16 v) {
+  return (u64)v.bits;
+}
+template <>
+__device__ __forceinline__ u64 to_bits<e4m3>(e4m3 v) {
+  return (u64)v.bits;
+}
+template <>
+__device__ __forceinline__ u64 to_bits<e5m2>(e5m2 v) {
   return (u64)v.bits;
 }
 
@@ -171,6 +230,16 @@ struct FloatTrait<f16> {
   static constexpr bool value = true;
   static constexpr bool half = true;
 };
+template <>
+struct FloatTrait<e4m3> {
+  static constexpr bool value = true;
+  static constexpr bool half = false;
+};
+template <>
+struct FloatTrait<e5m2> {
+  static constexpr bool value = true;
+  static constexpr bool half = false;
+};
 template <class T>
 __host__ __device__ constexpr bool is_float() {
   return FloatTrait<T>::value;
@@ -178,6 +247,15 @@ __host__ __device__ constexpr bool is_float() {
 template <class T>
 __host__ __device__ constexpr bool is_half() {
   return FloatTrait<T>::half;
+}
+template <class T>
+__host__ __device__ constexpr bool is_fp8() {
+  return std::is_same<T, e4m3>::value || std::is_same<T, e5m2>::value;
+}
+// bit-pattern storage types whose values are handled widened to f32
+template <class T>
+__host__ __device__ constexpr bool is_narrow() {
+  return is_half<T>() || is_fp8<T>();
 }
 
 // ---- 16-bit conversions: widening is exact; narrowing rounds once (RNE) --------
@@ -203,28 +281,83 @@ template <>
 __device__ __forceinline__ f16 half_from_f64<f16>(double x) {
   return f16(__half_as_ushort(__double2half(x)), true);  // F2F.F16.F64
 }
+// ---- 8-bit conversions: decoding is exact (every E4M3 / E5M2 value is an f16
+// value); encoding is cvt.rn.satfinite (nearest-even, overflow and +-inf to the
+// largest finite magnitude, NaN to NaN) ----------------------------------------
+__device__ __forceinline__ float to_f32(e4m3 v) {
+  unsigned h2;
+  asm("cvt.rn.f16x2.e4m3x2 %0, %1;" : "=r"(h2) : "h"((unsigned short)v.bits));
+  return __half2float(__ushort_as_half((unsigned short)(h2 & 0xffffu)));
+}
+__device__ __forceinline__ float to_f32(e5m2 v) {  // E5M2 = the top byte of an f16
+  return __half2float(__ushort_as_half((unsigned short)((unsigned)v.bits << 8)));
+}
+template <class H>
+__device__ __forceinline__ H fp8_from_f32(float x) {
+  unsigned short p;
+  if constexpr (std::is_same<H, e4m3>::value)
+    asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(p) : "f"(0.0f), "f"(x));
+  else
+    asm("cvt.rn.satfinite.e5m2x2.f32 %0, %1, %2;" : "=h"(p) : "f"(0.0f), "f"(x));
+  return H((unsigned char)(p & 0xffu), true);
+}
 // exact value of any element type as f64 (floats only are used)
 __device__ __forceinline__ double as_double(float v) { return (double)v; }
 __device__ __forceinline__ double as_double(double v) { return v; }
 __device__ __forceinline__ double as_double(bf16 v) { return (double)to_f32(v); }
 __device__ __forceinline__ double as_double(f16 v) { return (double)to_f32(v); }
+__device__ __forceinline__ double as_double(e4m3 v) { return (double)to_f32(v); }
+__device__ __forceinline__ double as_double(e5m2 v) { return (double)to_f32(v); }
 __device__ __forceinline__ double as_double(uint32_t v) { return (double)v; }
 __device__ __forceinline__ double as_double(s64 v) { return (double)v; }
-// exact value of an f32 / 16-bit element as f32
+// exact value of an f32 / 16-bit / 8-bit element as f32
 __device__ __forceinline__ float as_float(float v) { return v; }
 __device__ __forceinline__ float as_float(bf16 v) { return to_f32(v); }
 __device__ __forceinline__ float as_float(f16 v) { return to_f32(v); }
+__device__ __forceinline__ float as_float(e4m3 v) { return to_f32(v); }
+__device__ __forceinline__ float as_float(e5m2 v) { return to_f32(v); }
 // ordering (IEEE semantics for floats)
 template <class T>
 __device__ __forceinline__ bool lt(T a, T b) {
-  if constexpr (is_half<T>()) return to_f32(a) < to_f32(b);
+  if constexpr (is_narrow<T>()) return to_f32(a) < to_f32(b);
   else return a < b;
 }
 // element loads bypassing L1 (operands may alias the output exactly)
 template <class T>
 __device__ __forceinline__ T ldcg_elem(const T* p) {
   if constexpr (is_half<T>()) return T(__ldcg(reinterpret_cast<const unsigned short*>(p)), true);
+  else if constexpr (is_fp8<T>()) return T(__ldcg(reinterpret_cast<const unsigned char*>(p)), true);
   else return __ldcg(p);
+}
+
+// ---- storage <-> arithmetic type (identity except for the 8-bit types) ------
+template <class T, int W>
+__device__ __forceinline__ void widen_vec(const T (&v)[W], typename ComputeT<T>::type (&c)[W]) {
+#pragma unroll
+  for (int w = 0; w < W; ++w) {
+    if constexpr (is_fp8<T>()) c[w] = to_f32(v[w]);
+    else c[w] = v[w];
+  }
+}
+// f32 -> 8-bit, two at a time (cvt.rn.satfinite.{e4m3x2,e5m2x2}.f32)
+template <class T, int W>
+__device__ __forceinline__ void narrow_vec(const typename ComputeT<T>::type (&c)[W], T (&v)[W]) {
+  if constexpr (is_fp8<T>()) {
+#pragma unroll
+    for (int w = 0; w + 1 < W; w += 2) {
+      unsigned short p;
+      if constexpr (std::is_same<T, e4m3>::value)
+        asm("cvt.rn.satfinite.e4m3x2.f32 %0, %1, %2;" : "=h"(p) : "f"(c[w + 1]), "f"(c[w]));
+      else
+        asm("cvt.rn.satfinite.e5m2x2.f32 %0, %1, %2;" : "=h"(p) : "f"(c[w + 1]), "f"(c[w]));
+      v[w] = T((unsigned char)(p & 0xffu), true);
+      v[w + 1] = T((unsigned char)(p >> 8), true);
+    }
+    if constexpr (W & 1) v[W - 1] = fp8_from_f32<T>(c[W - 1]);
+  } else {
+#pragma unroll
+    for (int w = 0; w < W; ++w) v[w] = c[w];
+  }
 }
 
 // ---- op legality (R9) -----------------------------------------------------
@@ -384,6 +517,18 @@ __device__ __forceinline__ bf16 bin(bf16 a, bf16 b) {
 template <int OP>
 __device__ __forceinline__ f16 bin(f16 a, f16 b) {
   return half_bin<OP, f16>(a, b);
+}
+// 8-bit storage types: only MIN / MAX are applied to stored values (by the
+// min/max accumulators); every other op runs on the f32 arithmetic type.
+template <int OP>
+__device__ __forceinline__ e4m3 bin(e4m3 a, e4m3 b) {
+  static_assert(OP == COOT_OP_MIN || OP == COOT_OP_MAX, "8-bit values are only compared");
+  return OP == COOT_OP_MIN ? (lt(b, a) ? b : a) : (lt(a, b) ? b : a);
+}
+template <int OP>
+__device__ __forceinline__ e5m2 bin(e5m2 a, e5m2 b) {
+  static_assert(OP == COOT_OP_MIN || OP == COOT_OP_MAX, "8-bit values are only compared");
+  return OP == COOT_OP_MIN ? (lt(b, a) ? b : a) : (lt(a, b) ? b : a);
 }
 template <int OP>
 __device__ __forceinline__ uint32_t un(uint32_t a) {
@@ -611,6 +756,12 @@ __device__ __forceinline__ bf16 shfl_xor(bf16 v, int m) {
 __device__ __forceinline__ f16 shfl_xor(f16 v, int m) {
   return f16((unsigned short)__shfl_xor_sync(0xffffffffu, (unsigned)v.bits, m), true);
 }
+__device__ __forceinline__ e4m3 shfl_xor(e4m3 v, int m) {
+  return e4m3((unsigned char)__shfl_xor_sync(0xffffffffu, (unsigned)v.bits, m), true);
+}
+__device__ __forceinline__ e5m2 shfl_xor(e5m2 v, int m) {
+  return e5m2((unsigned char)__shfl_xor_sync(0xffffffffu, (unsigned)v.bits, m), true);
+}
 
 // ---- per-thread accumulators -------------------------------------------------
 template <class T>
@@ -644,6 +795,16 @@ template <>
 struct MinMaxId<f16> {
   __device__ static f16 lo() { return f16(0x7c00, true); }
   __device__ static f16 hi() { return f16(0xfc00, true); }
+};
+template <>
+struct MinMaxId<e4m3> {  // no infinities: the largest finite magnitudes (+-448)
+  __device__ static e4m3 lo() { return e4m3(0x7e, true); }
+  __device__ static e4m3 hi() { return e4m3(0xfe, true); }
+};
+template <>
+struct MinMaxId<e5m2> {  // +-inf
+  __device__ static e5m2 lo() { return e5m2(0x7c, true); }
+  __device__ static e5m2 hi() { return e5m2(0xfc, true); }
 };
 
 // Sum type: f64 for floats, u64 (modular) for integers.
@@ -688,9 +849,10 @@ __device__ __forceinline__ float pairwise_f32(const float (&x)[W]) {
 
 template <class T, int W>
 __device__ __forceinline__ typename SumT<T>::type unit_sum(const T (&v)[W]) {
-  if constexpr (is_half<T>()) {
+  if constexpr (is_narrow<T>()) {
     // widen exactly, pairwise sum in f32 (error ~2^-24, far below the format's
-    // 2^-9 / 2^-12 rounding), one conversion to f64 per unit
+    // 2^-9 / 2^-12 rounding; E4M3 unit sums are exact), one conversion to f64
+    // per unit
     float x[W];
 #pragma unroll
     for (int w = 0; w < W; ++w) x[w] = to_f32(v[w]);
@@ -794,7 +956,7 @@ struct Accum {
     } else if constexpr (ACC == ACC_SUM) {
       s = sum_add<S>(s, unit_sum<T, W>(v));
     } else if constexpr (ACC == ACC_SUMSQ) {
-      if constexpr (is_half<T>()) {  // squares of 16-bit values are exact in f32
+      if constexpr (is_narrow<T>()) {  // squares of 16/8-bit values are exact in f32
         float q[W];
 #pragma unroll
         for (int w = 0; w < W; ++w) {
@@ -938,36 +1100,44 @@ __device__ __forceinline__ T round_to(double x) {
   else return (T)x;
 }
 
-// Round the combined accumulator into the user-visible result (eT, or a u64
-// index).  `count` = number of elements reduced (MEAN's divisor).
+// the result-type value of an element (exact: the 8-bit types widen to f32)
+template <class T>
+__device__ __forceinline__ typename ResultT<T>::type as_result(T v) {
+  if constexpr (is_fp8<T>()) return to_f32(v);
+  else return v;
+}
+
+// Round the combined accumulator into the user-visible result (ResultT<eT>,
+// or a u64 index).  `count` = number of elements reduced (MEAN's divisor).
 template <class T, int ACC>
 __device__ __forceinline__ void write_final(const Accum<T, ACC>& acc, uint32_t kind, void* result,
                                             u64 count) {
-  T* out = reinterpret_cast<T*>(result);
+  typedef typename ResultT<T>::type R;
+  R* out = reinterpret_cast<R*>(result);
   if constexpr (ACC == ACC_VAR) {
     const double var = acc.n > 1 ? __ddiv_rn(acc.s2 - __ddiv_rn(__dmul_rn(acc.s1, acc.s1),
                                                                 (double)acc.n),
                                              (double)(acc.n - 1))
                                  : 0.0;
     const double v = var > 0.0 ? var : 0.0;
-    out[0] = round_to<T>(kind == COOT_RED_STDDEV ? __dsqrt_rn(v) : v);
+    out[0] = round_to<R>(kind == COOT_RED_STDDEV ? __dsqrt_rn(v) : v);
   } else if constexpr (ACC == ACC_IMIN || ACC == ACC_IMAX) {
     *reinterpret_cast<u64*>(result) = acc.idx;
   } else if constexpr (ACC == ACC_SUM && is_float<T>()) {
-    if (kind == COOT_RED_MEAN) out[0] = round_to<T>(__ddiv_rn(acc.s, (double)count));
-    else out[0] = round_to<T>(acc.s);
+    if (kind == COOT_RED_MEAN) out[0] = round_to<R>(__ddiv_rn(acc.s, (double)count));
+    else out[0] = round_to<R>(acc.s);
   } else if constexpr (ACC == ACC_MINMAX) {
-    if (kind == COOT_RED_MIN) out[0] = acc.mn;
-    else if (kind == COOT_RED_MAX) out[0] = acc.mx;
+    if (kind == COOT_RED_MIN) out[0] = as_result(acc.mn);
+    else if (kind == COOT_RED_MAX) out[0] = as_result(acc.mx);
     else {
-      out[0] = acc.mn;
-      out[1] = acc.mx;
+      out[0] = as_result(acc.mn);
+      out[1] = as_result(acc.mx);
     }
   } else if constexpr (ACC == ACC_SUMSQ) {
-    out[0] = round_to<T>(__dsqrt_rn(acc.s));
+    out[0] = round_to<R>(__dsqrt_rn(acc.s));
   } else if constexpr (ACC == ACC_SUM) {
     if constexpr (is_float<T>()) {
-      out[0] = round_to<T>(acc.s);
+      out[0] = round_to<R>(acc.s);
     } else {
       out[0] = (T)acc.s;  // modular truncation for u32
     }

@@ -39,10 +39,11 @@ __device__ __forceinline__ void store_dim_value(const DimArgs& d, u64 idx,
   if (d.final_mode == FINAL_PARTIAL) {
     reinterpret_cast<S*>(d.result)[idx] = s;
   } else {
-    T v;
-    if constexpr (is_float<T>()) v = round_to<T>(s);
-    else v = (T)s;
-    reinterpret_cast<T*>(d.result)[idx] = v;
+    typedef typename ResultT<T>::type R;  // f32 for the 8-bit storage types
+    R v;
+    if constexpr (is_float<T>()) v = round_to<R>(s);
+    else v = (R)s;
+    reinterpret_cast<R*>(d.result)[idx] = v;
   }
 }
 

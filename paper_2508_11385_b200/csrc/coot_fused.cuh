@@ -88,19 +88,36 @@ struct StaticProg {
   }
 };
 
+// LOAD into the arithmetic-type stack (a plain copy unless T is an 8-bit
+// storage type, which is decoded to f32).
+template <class T, int W, class Src>
+__device__ __forceinline__ void load_to(const Src& src, int k,
+                                        typename ComputeT<T>::type (&dst)[W]) {
+  if constexpr (std::is_same<typename ComputeT<T>::type, T>::value) {
+    src.get(k, dst);
+  } else {
+    T raw[W];
+    src.get(k, raw);
+    widen_vec<T, W>(raw, dst);
+  }
+}
+
+// The stack holds ComputeT<T> (T itself except for the 8-bit storage types,
+// whose programs run in f32); results are narrowed back to T at the end.
 template <class T, int W, int SP, int C, int... Rest>
 struct StaticStep {
+  typedef typename ComputeT<T>::type CT;
   template <class Src>
-  __device__ __forceinline__ static void run(T (&st)[COOT_MAX_STACK][W], const Src& src,
+  __device__ __forceinline__ static void run(CT (&st)[COOT_MAX_STACK][W], const Src& src,
                                              const FusedArgs& a) {
     constexpr int op = ins_op(C), arg = ins_arg(C);
     constexpr int nsp = (op == COOT_OP_LOAD || op == COOT_OP_SCALAR) ? SP + 1
                         : is_unary_op(op)                            ? SP
                                                                      : SP - 1;
     if constexpr (op == COOT_OP_LOAD) {
-      src.template get_c<arg>(st[SP]);
+      load_to<T, W>(src, arg, st[SP]);
     } else if constexpr (op == COOT_OP_SCALAR) {
-      const T s = scalar_as<T>(a.scalars[arg]);
+      const CT s = scalar_as<CT>(a.scalars[arg]);
 #pragma unroll
       for (int w = 0; w < W; ++w) st[SP][w] = s;
     } else if constexpr (is_unary_op(op)) {
@@ -120,10 +137,9 @@ struct CatalogEval<StaticProg<Code...>> {
   static constexpr bool kInterp = false;
   template <class T, int W, class Src>
   __device__ __forceinline__ static void eval_src(const Src& src, const FusedArgs& a, T (&out)[W]) {
-    T st[COOT_MAX_STACK][W];
+    typename ComputeT<T>::type st[COOT_MAX_STACK][W];
     StaticStep<T, W, 0, Code...>::run(st, src, a);
-#pragma unroll
-    for (int w = 0; w < W; ++w) out[w] = st[0][w];
+    narrow_vec<T, W>(st[0], out);
   }
   template <class T, int W>
   __device__ __forceinline__ static void eval(const T (&in)[K][W], const FusedArgs& a, T (&out)[W]) {
@@ -148,16 +164,17 @@ struct InterpEval {
 
   template <class T, int W, class Src>
   __device__ __forceinline__ static void eval_src(const Src& src, const FusedArgs& a, T (&out)[W]) {
-    T st[SMAX][W];  // every slot is written (LOAD/SCALAR) before it is read
+    typedef typename ComputeT<T>::type CT;
+    CT st[SMAX][W];  // every slot is written (LOAD/SCALAR) before it is read
 
 #define COOT_LOAD_CASE(d)                                                  \
   case COOT_KEY(COOT_OP_LOAD, d):                                          \
-    if constexpr ((d) < SMAX) src.get((int)a.arg[i], st[(d) < SMAX ? (d) : 0]); \
+    if constexpr ((d) < SMAX) load_to<T, W>(src, (int)a.arg[i], st[(d) < SMAX ? (d) : 0]); \
     break;
 #define COOT_SCALAR_CASE(d)                                                \
   case COOT_KEY(COOT_OP_SCALAR, d):                                        \
     if constexpr ((d) < SMAX) {                                            \
-      const T s = scalar_as<T>(a.scalars[a.arg[i]]);                       \
+      const CT s = scalar_as<CT>(a.scalars[a.arg[i]]);                     \
       _Pragma("unroll") for (int w = 0; w < W; ++w) st[d][w] = s;          \
     }                                                                      \
     break;
@@ -202,8 +219,7 @@ struct InterpEval {
 #undef COOT_UN_CASE
 #undef COOT_SCALAR_CASE
 #undef COOT_LOAD_CASE
-#pragma unroll
-    for (int w = 0; w < W; ++w) out[w] = st[0][w];
+    narrow_vec<T, W>(st[0], out);
   }
   template <class T, int W>
   __device__ __forceinline__ static void eval(const T (&in)[K][W], const FusedArgs& a, T (&out)[W]) {

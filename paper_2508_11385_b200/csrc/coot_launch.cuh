@@ -187,14 +187,15 @@ __global__ void combine_rec_kernel(const Rec* parts, uint32_t nparts, uint32_t k
 // Vector partials (SUM_DIM*): result[i] = round(sum_p parts[p][i]), p in order.
 template <class T>
 __global__ void combine_vec_kernel(const typename SumT<T>::type* parts, uint32_t nparts, u64 len,
-                                   T* result) {
+                                   typename ResultT<T>::type* result) {
   typedef typename SumT<T>::type S;
+  typedef typename ResultT<T>::type R;
   for (u64 i = (u64)blockIdx.x * blockDim.x + threadIdx.x; i < len;
        i += (u64)gridDim.x * blockDim.x) {
     S s = S(0);
     for (uint32_t p = 0; p < nparts; ++p) s = sum_add<S>(s, parts[(u64)p * len + i]);
-    if constexpr (is_float<T>()) result[i] = round_to<T>(s);
-    else result[i] = (T)s;
+    if constexpr (is_float<T>()) result[i] = round_to<R>(s);
+    else result[i] = (R)s;
   }
 }
 
@@ -212,7 +213,7 @@ cudaError_t launch_combine_t(uint32_t kind, int acc, const void* parts, uint32_t
   if (kind == COOT_RED_SUM_DIM0 || kind == COOT_RED_SUM_DIM1) {
     combine_vec_kernel<T><<<grid, kThreads, 0, s>>>(
         reinterpret_cast<const typename SumT<T>::type*>(parts), nparts, len,
-        reinterpret_cast<T*>(result));
+        reinterpret_cast<typename ResultT<T>::type*>(result));
     return cudaGetLastError();
   }
   const Rec* r = reinterpret_cast<const Rec*>(parts);
@@ -288,6 +289,8 @@ __global__ void fill_kernel(uint32_t kind, u64 seed, u64 stream, u64 start, u64 
       const u64 h = splitmix_mix(key + (g + 1) * 0x9E3779B97F4A7C15ull);
       if constexpr (std::is_same<T, bf16>::value) v = half_from_f32<bf16>((float)(h >> 56) * 0x1p-8f);
       else if constexpr (std::is_same<T, f16>::value) v = half_from_f32<f16>((float)(h >> 53) * 0x1p-11f);
+      else if constexpr (std::is_same<T, e4m3>::value) v = fp8_from_f32<e4m3>((float)(h >> 60) * 0x1p-4f);
+      else if constexpr (std::is_same<T, e5m2>::value) v = fp8_from_f32<e5m2>((float)(h >> 61) * 0x1p-3f);
       else if constexpr (sizeof(T) == 4 && is_float<T>()) v = (float)(h >> 40) * 0x1p-24f;
       else if constexpr (is_float<T>()) v = (double)(h >> 11) * 0x1p-53;
       else if constexpr (sizeof(T) == 4) v = (T)(h >> 32);
@@ -303,6 +306,7 @@ __global__ void fill_kernel(uint32_t kind, u64 seed, u64 stream, u64 start, u64 
         default: iv = 0; break;
       }
       if constexpr (is_half<T>()) v = half_from_f64<T>((double)iv);
+      else if constexpr (is_fp8<T>()) v = fp8_from_f32<T>((float)iv);  // exact below 2^24; saturates far sooner
       else v = (T)iv;
     }
     out[i] = v;

@@ -78,12 +78,20 @@ size_t elem_size(uint32_t elem) {
     case COOT_S64: return 8;
     case COOT_BF16: return 2;
     case COOT_F16: return 2;
+    case COOT_E4M3: return 1;
+    case COOT_E5M2: return 1;
   }
   return 0;
 }
 
+// size of one reduction / dim-sum result element (f32 for the 8-bit types, R25)
+size_t result_elem_size(uint32_t elem) {
+  return (elem == COOT_E4M3 || elem == COOT_E5M2) ? 4 : elem_size(elem);
+}
+
 bool is_float_elem(uint32_t e) {
-  return e == COOT_F32 || e == COOT_F64 || e == COOT_BF16 || e == COOT_F16;
+  return e == COOT_F32 || e == COOT_F64 || e == COOT_BF16 || e == COOT_F16 || e == COOT_E4M3 ||
+         e == COOT_E5M2;
 }
 bool is_unary(int op) { return op >= COOT_OP_NEG && op <= COOT_OP_LOG; }
 bool is_binary(int op) { return op >= COOT_OP_ADD && op <= COOT_OP_MAX; }
@@ -364,6 +372,8 @@ cudaError_t dispatch_fused(uint32_t elem, const coot::FusedPlan& p, const coot::
     case COOT_S64: return coot::launch_fused_t<coot::s64>(p, a, s);
     case COOT_BF16: return coot::launch_fused_t<coot::bf16>(p, a, s);
     case COOT_F16: return coot::launch_fused_t<coot::f16>(p, a, s);
+    case COOT_E4M3: return coot::launch_fused_t<coot::e4m3>(p, a, s);
+    case COOT_E5M2: return coot::launch_fused_t<coot::e5m2>(p, a, s);
   }
   return cudaErrorInvalidValue;
 }
@@ -377,6 +387,8 @@ cudaError_t dispatch_dim(uint32_t elem, const coot::DimPlan& p, const coot::DimA
     case COOT_S64: return coot::launch_dim_t<coot::s64>(p, a, s);
     case COOT_BF16: return coot::launch_dim_t<coot::bf16>(p, a, s);
     case COOT_F16: return coot::launch_dim_t<coot::f16>(p, a, s);
+    case COOT_E4M3: return coot::launch_dim_t<coot::e4m3>(p, a, s);
+    case COOT_E5M2: return coot::launch_dim_t<coot::e5m2>(p, a, s);
   }
   return cudaErrorInvalidValue;
 }
@@ -763,7 +775,7 @@ coot_status reduce_common(coot_ctx* ctx, const coot_expr* e, uint32_t kind, void
   const coot_operand outv = dense_view(out, e->n_rows, e->n_cols);
   st = check_out_alias(e, out ? &outv : nullptr);
   if (st != COOT_OK) return st;
-  size_t rbytes = result_bytes(kind, es, e->n_rows, e->n_cols);
+  size_t rbytes = result_bytes(kind, result_elem_size(e->elem), e->n_rows, e->n_cols);
   if (final_mode == coot::FINAL_PARTIAL)
     rbytes = dim ? (kind == COOT_RED_SUM_DIM0 ? e->n_cols : e->n_rows) * 8 : COOT_PARTIAL_BYTES;
   st = check_result_alias(e, result, rbytes, out ? &outv : nullptr);
@@ -782,13 +794,15 @@ coot_status reduce_common(coot_ctx* ctx, const coot_expr* e, uint32_t kind, void
         case COOT_U32: cerr = coot::launch_empty_rec_t<uint32_t>(acc, result, ctx->stream); break;
         case COOT_BF16: cerr = coot::launch_empty_rec_t<coot::bf16>(acc, result, ctx->stream); break;
         case COOT_F16: cerr = coot::launch_empty_rec_t<coot::f16>(acc, result, ctx->stream); break;
+        case COOT_E4M3: cerr = coot::launch_empty_rec_t<coot::e4m3>(acc, result, ctx->stream); break;
+        case COOT_E5M2: cerr = coot::launch_empty_rec_t<coot::e5m2>(acc, result, ctx->stream); break;
         default: cerr = coot::launch_empty_rec_t<coot::s64>(acc, result, ctx->stream); break;
       }
       if (cerr != cudaSuccess) return cuda_fail(cerr, "empty record launch");
       ctx->stats.launches++;
       return ok();
     }
-    cudaError_t cerr = cudaMemsetAsync(result, 0, es, ctx->stream);  // ACCU / NORM2 of empty = 0
+    cudaError_t cerr = cudaMemsetAsync(result, 0, result_elem_size(e->elem), ctx->stream);  // ACCU / NORM2 of empty = 0
     if (cerr != cudaSuccess) return cuda_fail(cerr, "cudaMemsetAsync");
     return ok();
   }
@@ -974,6 +988,8 @@ coot_status coot_combine(coot_ctx* ctx, uint32_t elem, uint32_t kind, const void
     case COOT_U32: ce = coot::launch_combine_t<uint32_t>(kind, acc, partials, nparts, len, result, grid, ctx->stream); break;
     case COOT_BF16: ce = coot::launch_combine_t<coot::bf16>(kind, acc, partials, nparts, len, result, grid, ctx->stream); break;
     case COOT_F16: ce = coot::launch_combine_t<coot::f16>(kind, acc, partials, nparts, len, result, grid, ctx->stream); break;
+    case COOT_E4M3: ce = coot::launch_combine_t<coot::e4m3>(kind, acc, partials, nparts, len, result, grid, ctx->stream); break;
+    case COOT_E5M2: ce = coot::launch_combine_t<coot::e5m2>(kind, acc, partials, nparts, len, result, grid, ctx->stream); break;
     default: ce = coot::launch_combine_t<coot::s64>(kind, acc, partials, nparts, len, result, grid, ctx->stream); break;
   }
   if (ce != cudaSuccess) return cuda_fail(ce, "combine kernel launch");
@@ -1019,6 +1035,8 @@ coot_status coot_fill(coot_ctx* ctx, uint32_t elem, uint32_t fill_kind, uint64_t
     case COOT_U32: ce = coot::launch_fill_t<uint32_t>(fill_kind, seed, stream, start, count, n_rows, k, out, grid, ctx->stream); break;
     case COOT_BF16: ce = coot::launch_fill_t<coot::bf16>(fill_kind, seed, stream, start, count, n_rows, k, out, grid, ctx->stream); break;
     case COOT_F16: ce = coot::launch_fill_t<coot::f16>(fill_kind, seed, stream, start, count, n_rows, k, out, grid, ctx->stream); break;
+    case COOT_E4M3: ce = coot::launch_fill_t<coot::e4m3>(fill_kind, seed, stream, start, count, n_rows, k, out, grid, ctx->stream); break;
+    case COOT_E5M2: ce = coot::launch_fill_t<coot::e5m2>(fill_kind, seed, stream, start, count, n_rows, k, out, grid, ctx->stream); break;
     default: ce = coot::launch_fill_t<coot::s64>(fill_kind, seed, stream, start, count, n_rows, k, out, grid, ctx->stream); break;
   }
   if (ce != cudaSuccess) return cuda_fail(ce, "fill kernel launch");

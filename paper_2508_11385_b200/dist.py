@@ -17,7 +17,7 @@ from __future__ import annotations
 import torch
 import torch.distributed as dist
 
-from .api import TORCH_DTYPE, Context, Lowered, partial_bytes, shard_range
+from .api import RESULT_DTYPE, Context, Lowered, partial_bytes, shard_range
 
 __all__ = ["shard_range", "column_block", "allgather_partials", "DistReducer"]
 
@@ -72,7 +72,7 @@ class DistReducer:
             e1.record(self.ctx.stream)
             kernel_events.append((e0, e1))
         parts = allgather_partials(self._rec, self.group)
-        dtype = torch.int64 if kind.startswith("INDEX") else TORCH_DTYPE[lw.elem]
+        dtype = torch.int64 if kind.startswith("INDEX") else RESULT_DTYPE[lw.elem]
         res = torch.empty(2, dtype=dtype, device=self.ctx.device)
         self.ctx.combine(lw.elem, kind, parts, self.world, 1, res)
         return res
@@ -86,14 +86,14 @@ class DistReducer:
         self.ctx.reduce_partial(lw.elem, lw.n_rows, lw.n_cols, lw.program, lw.operands,
                                 lw.scalars, "SUM_DIM1", part)
         parts = allgather_partials(part, self.group)
-        res = torch.empty(m, dtype=TORCH_DTYPE[lw.elem], device=self.ctx.device)
+        res = torch.empty(m, dtype=RESULT_DTYPE[lw.elem], device=self.ctx.device)
         self.ctx.combine(lw.elem, "SUM_DIM1", parts, self.world, m, res)
         return res
 
     def sum_dim0_columns(self, lw: Lowered) -> torch.Tensor:
         """sum(X, 0) when ranks own column blocks: purely local (no exchange);
         returns this rank's slice of the Row."""
-        res = torch.empty(lw.n_cols, dtype=TORCH_DTYPE[lw.elem], device=self.ctx.device)
+        res = torch.empty(lw.n_cols, dtype=RESULT_DTYPE[lw.elem], device=self.ctx.device)
         self.ctx.reduce(lw.elem, lw.n_rows, lw.n_cols, lw.program, lw.operands, lw.scalars,
                         "SUM_DIM0", res)
         return res

@@ -6,7 +6,9 @@ import pytest
 import torch
 
 TORCH = {"f32": torch.float32, "f64": torch.float64, "u32": torch.uint32, "s64": torch.int64,
-         "bf16": torch.bfloat16, "f16": torch.float16}
+         "bf16": torch.bfloat16, "f16": torch.float16,
+         "e4m3": torch.float8_e4m3fn, "e5m2": torch.float8_e5m2}
+RTORCH = dict(TORCH, e4m3=torch.float32, e5m2=torch.float32)  # reduction result dtypes
 
 
 def have_gpu() -> bool:
@@ -24,6 +26,8 @@ def to_dev(a: np.ndarray, etype: str, offset: int = 0) -> torch.Tensor:
         t = torch.from_numpy(a.view(np.int32).copy()).view(torch.uint32)
     elif etype == "bf16":  # host arrays hold bf16 bit patterns (uint16)
         t = torch.from_numpy(a.view(np.int16).copy()).view(torch.bfloat16)
+    elif etype in ("e4m3", "e5m2"):  # host arrays hold 8-bit patterns (uint8)
+        t = torch.from_numpy(a.copy()).view(TORCH[etype])
     else:
         t = torch.from_numpy(a.copy())
     base = torch.empty(a.size + offset + 8, dtype=TORCH[etype], device="cuda")
@@ -34,7 +38,7 @@ def to_dev(a: np.ndarray, etype: str, offset: int = 0) -> torch.Tensor:
 
 def _np_view(etype):
     return {"f32": np.float32, "f64": np.float64, "u32": np.uint32, "s64": np.int64,
-            "bf16": np.uint16, "f16": np.float16}[etype]
+            "bf16": np.uint16, "f16": np.float16, "e4m3": np.uint8, "e5m2": np.uint8}[etype]
 
 
 def empty_dev(n: int, etype: str, offset: int = 0) -> torch.Tensor:
@@ -47,6 +51,8 @@ def to_host(t: torch.Tensor, etype: str) -> np.ndarray:
         return t.cpu().view(torch.int32).numpy().view(np.uint32)
     if etype == "bf16":
         return t.cpu().view(torch.int16).numpy().view(np.uint16)
+    if etype in ("e4m3", "e5m2") and t.dtype == TORCH[etype]:
+        return t.cpu().view(torch.uint8).numpy()
     return t.cpu().numpy()
 
 

@@ -53,7 +53,12 @@ WL = {
     "f16_axpy_eval_2p30": ("f16", 1 << 30, 1, "S0 L0 MUL L1 ADD", [2.5], None, True, False),
     "bf16_var_2p31": ("bf16", 1 << 31, 1, "L0", [], "VAR", False, False),
     "bf16_dim0": ("bf16", 32768, 32768, "L0", [], "SUM_DIM0", False, False),
-    "bf16_interp_c2": ("bf16", 1 << 30, 1, "L0 L1 MUL EXP S0 L2 MUL ADD", [3.0], "ACCU", True, True),
+    "e4m3_c2_2p32": ("e4m3", 1 << 32, 1, "L0 L1 MUL EXP S0 L2 MUL ADD", [3.0], "ACCU", False, False),
+    "e4m3_c2_eval_2p31": ("e4m3", 1 << 31, 1, "L0 L1 MUL EXP S0 L2 MUL ADD", [3.0], "ACCU", True, False),
+    "e5m2_axpy_eval_2p31": ("e5m2", 1 << 31, 1, "S0 L0 MUL L1 ADD", [2.5], None, True, False),
+    "e4m3_dot_2p32": ("e4m3", 1 << 32, 1, "L0 L1 MUL", [], "ACCU", False, False),
+    "e4m3_dim1": ("e4m3", 65536, 32768, "L0", [], "SUM_DIM1", False, False),
+    "bf16_interp_c2":("bf16", 1 << 30, 1, "L0 L1 MUL EXP S0 L2 MUL ADD", [3.0], "ACCU", True, True),
 }
 
 
@@ -80,7 +85,8 @@ def run(name, reps, ctxs):
             ctx.fill(t, "randu", stream=s, n_rows=m)
         out = torch.empty(m * n, dtype=dt, device="cuda") if store else None
     rlen = n if kind == "SUM_DIM0" else (m if kind == "SUM_DIM1" else 2)
-    res = torch.empty(rlen, dtype=torch.int64 if kind and kind.startswith("INDEX") else dt,
+    res = torch.empty(rlen, dtype=torch.int64 if kind and kind.startswith("INDEX")
+                      else api.RESULT_DTYPE[elem],
                       device="cuda")
 
     def call():
@@ -101,7 +107,7 @@ def run(name, reps, ctxs):
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / reps
-    rbytes = (n if kind == "SUM_DIM0" else m if kind == "SUM_DIM1" else 0) * es
+    rbytes = (n if kind == "SUM_DIM0" else m if kind == "SUM_DIM1" else 0) * res.element_size()
     alg = m * n * es * (k + (1 if store in (True, "diag") else 0)) + rbytes
     st = ctx.stats()
     del ops, out
