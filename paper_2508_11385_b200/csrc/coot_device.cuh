@@ -330,13 +330,47 @@ __device__ __forceinline__ T ldcg_elem(const T* p) {
   else return __ldcg(p);
 }
 
+// Two 8-bit values -> two f32, exactly: one cvt.rn.f16x2.{e4m3x2,e5m2x2}
+// (E5M2 is a byte permute) and a paired f16 -> f32 widening.
+template <class T>
+__device__ __forceinline__ float2 fp8x2_to_f32x2(T lo, T hi) {
+  const unsigned short pk = (unsigned short)(lo.bits | ((unsigned)hi.bits << 8));
+  unsigned h2;
+  if constexpr (std::is_same<T, e4m3>::value) {
+    asm("cvt.rn.f16x2.e4m3x2 %0, %1;" : "=r"(h2) : "h"(pk));
+  } else {
+    h2 = __byte_perm((unsigned)pk, 0u, 0x1404);  // bytes -> the high byte of each f16
+  }
+  __half2 h;
+  memcpy(&h, &h2, 4);
+  return __half22float2(h);
+}
+
+// Exact f32 values of W f32 / 16-bit / 8-bit elements (8-bit: pairwise).
+template <class T, int W>
+__device__ __forceinline__ void widen_f32(const T (&v)[W], float (&x)[W]) {
+  if constexpr (is_fp8<T>()) {
+#pragma unroll
+    for (int w = 0; w + 1 < W; w += 2) {
+      const float2 f = fp8x2_to_f32x2(v[w], v[w + 1]);
+      x[w] = f.x;
+      x[w + 1] = f.y;
+    }
+    if constexpr (W & 1) x[W - 1] = to_f32(v[W - 1]);
+  } else {
+#pragma unroll
+    for (int w = 0; w < W; ++w) x[w] = as_float(v[w]);
+  }
+}
+
 // ---- storage <-> arithmetic type (identity except for the 8-bit types) ------
 template <class T, int W>
 __device__ __forceinline__ void widen_vec(const T (&v)[W], typename ComputeT<T>::type (&c)[W]) {
+  if constexpr (is_fp8<T>()) {
+    widen_f32<T, W>(v, c);
+  } else {
 #pragma unroll
-  for (int w = 0; w < W; ++w) {
-    if constexpr (is_fp8<T>()) c[w] = to_f32(v[w]);
-    else c[w] = v[w];
+    for (int w = 0; w < W; ++w) c[w] = v[w];
   }
 }
 // f32 -> 8-bit, two at a time (cvt.rn.satfinite.{e4m3x2,e5m2x2}.f32)
@@ -854,8 +888,7 @@ __device__ __forceinline__ typename SumT<T>::type unit_sum(const T (&v)[W]) {
     // 2^-9 / 2^-12 rounding; E4M3 unit sums are exact), one conversion to f64
     // per unit
     float x[W];
-#pragma unroll
-    for (int w = 0; w < W; ++w) x[w] = to_f32(v[w]);
+    widen_f32<T, W>(v, x);
     return (double)pairwise_f32<W>(x);
   } else if constexpr (is_float<T>()) {
     if constexpr (W == 1) {
@@ -942,10 +975,11 @@ struct Accum {
         // so exact in f32; x - c is exact when x is near c), widened to f64 once
         // per unit — relative error ~W * 2^-24, far inside the 1e-5 bar
         const float cf = (float)c;
-        float a1 = 0.f, a2 = 0.f;
+        float a1 = 0.f, a2 = 0.f, x[W];
+        widen_f32<T, W>(v, x);
 #pragma unroll
         for (int w = 0; w < W; ++w) {
-          const float d = __fsub_rn(as_float(v[w]), cf);
+          const float d = __fsub_rn(x[w], cf);
           a1 = __fadd_rn(a1, d);
           a2 = __fmaf_rn(d, d, a2);
         }
@@ -958,11 +992,9 @@ struct Accum {
     } else if constexpr (ACC == ACC_SUMSQ) {
       if constexpr (is_narrow<T>()) {  // squares of 16/8-bit values are exact in f32
         float q[W];
+        widen_f32<T, W>(v, q);
 #pragma unroll
-        for (int w = 0; w < W; ++w) {
-          const float x = to_f32(v[w]);
-          q[w] = __fmul_rn(x, x);
-        }
+        for (int w = 0; w < W; ++w) q[w] = __fmul_rn(q[w], q[w]);
         s = sum_add<S>(s, (double)pairwise_f32<W>(q));
       } else {
         T q[W];
