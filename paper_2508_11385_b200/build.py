@@ -4,14 +4,20 @@ Flags: -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo, and the
 numerics contract of DESIGN.md R5/R7: -fmad=false (no FMA contraction),
 -ftz=false, -prec-div=true, -prec-sqrt=true.  cudart is linked statically so
 the library only needs the driver at run time.
+
+Incremental: a translation unit is recompiled when its source or any header
+(or this file) is newer than its object; each object is stamped with the time
+its compile STARTED, so an edit made while a build is running is never masked.
 """
 from __future__ import annotations
 
 import concurrent.futures as cf
 import glob
+import json
 import os
 import subprocess
 import sys
+import time
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
@@ -32,26 +38,55 @@ def _sources():
     return sorted(glob.glob(os.path.join(CSRC, "*.cu")))
 
 
-def _deps():
-    return _sources() + glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(CSRC, "*.h")) \
-        + [os.path.join(INCLUDE, "coot.h"), os.path.abspath(__file__)]
+def _headers():
+    return (glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(CSRC, "*.h"))
+            + glob.glob(os.path.join(CSRC, "*.inc"))
+            + [os.path.join(INCLUDE, "coot.h"), os.path.abspath(__file__)])
+
+
+def _obj(src: str) -> str:
+    return os.path.join(BUILD, os.path.basename(src) + ".o")
+
+
+def _stale(src: str, newest_header: float) -> bool:
+    obj = _obj(src)
+    if not os.path.exists(obj):
+        return True
+    t = os.path.getmtime(obj)
+    return os.path.getmtime(src) > t or newest_header > t
+
+
+STAMP = LIB + ".objs.json"  # object mtimes the library was linked from
+
+
+def _obj_times() -> dict:
+    return {os.path.basename(s): os.path.getmtime(_obj(s)) for s in _sources()}
 
 
 def up_to_date() -> bool:
     if not os.path.exists(LIB):
         return False
+    srcs = _sources()
+    if os.path.exists(STAMP) and all(os.path.exists(_obj(s)) for s in srcs):
+        hdr = max(os.path.getmtime(h) for h in _headers())
+        with open(STAMP) as f:
+            linked = json.load(f)
+        return not any(_stale(s, hdr) for s in srcs) and linked == _obj_times()
+    # no object tree (e.g. a copy of the repo without build/): compare sources
     t = os.path.getmtime(LIB)
-    return all(os.path.getmtime(d) <= t for d in _deps())
+    return all(os.path.getmtime(d) <= t for d in srcs + _headers())
 
 
 def _compile(src: str) -> str:
-    obj = os.path.join(BUILD, os.path.basename(src) + ".o")
+    obj = _obj(src)
+    started = time.time()
     cmd = [NVCC, *ARCH, *FLAGS, "-c", src, "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc failed for {src}:\n{r.stdout}\n{r.stderr}")
     if r.stderr.strip():
         sys.stderr.write(r.stderr)
+    os.utime(obj, (started, started))  # an edit during this compile stays "newer"
     return obj
 
 
@@ -60,13 +95,23 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return LIB
     os.makedirs(BUILD, exist_ok=True)
     srcs = _sources()
-    with cf.ThreadPoolExecutor(max_workers=max(1, min(len(srcs), os.cpu_count() or 4))) as ex:
-        objs = list(ex.map(_compile, srcs))
+    hdr = max(os.path.getmtime(h) for h in _headers())
+    todo = [s for s in srcs if force or _stale(s, hdr)]
+    if todo:
+        with cf.ThreadPoolExecutor(max_workers=max(1, min(len(todo), os.cpu_count() or 4))) as ex:
+            list(ex.map(_compile, todo))
+    objs = [_obj(s) for s in srcs]
     tmp = LIB + ".tmp"
     subprocess.check_call([NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-Xcompiler", "-fPIC"])
+    # the library is stamped as old as its oldest object, so a header edited
+    # during this build still makes up_to_date() false next time
+    oldest = min(os.path.getmtime(o) for o in objs)
     os.replace(tmp, LIB)
+    os.utime(LIB, (oldest, oldest))
+    with open(STAMP, "w") as f:
+        json.dump(_obj_times(), f)
     if verbose:
-        print(f"built {LIB}")
+        print(f"built {LIB} ({len(todo)} of {len(srcs)} units compiled)")
     return LIB
 
 

@@ -100,7 +100,7 @@ __global__ void __launch_bounds__(kTmaThreads, tma_min_ctas<EV>()) dim0_tma_kern
     }
   } else {
   // consumers (named barrier 1 synchronises the 256 consumer threads only)
-  constexpr int UD = units_per_dispatch<EV>();
+  constexpr int UD = units_per_dispatch<T, EV>();
   uint32_t s = 0, ph = 0;
   for (u64 p = blockIdx.x; p < npieces; p += gridDim.x) {
     const u64 j = p / d.nseg, r0 = (p % d.nseg) * d.seg_len;

@@ -148,13 +148,14 @@ struct CatalogEval<StaticProg<Code...>> {
 };
 
 // ---- K2: warp-uniform register interpreter --------------------------------
-// The host precomputes a dense key = op * 9 + depth for every instruction
-// (depth = stack size before it, 0..8).  Keys live in the kernel's parameter
-// bank and are uniform across the grid, so each `switch` (a jump table over
-// 126 dense cases) is a uniform branch; every case touches stack registers
-// with compile-time indices.  LOAD takes its operand index at run time from
-// the source (a shared-memory address under the TMA driver).  One dispatch
-// evaluates a whole 16-byte unit.
+// The host precomputes a key = op * 9 + depth for every instruction (depth =
+// stack size before it, 0..8).  Keys live in the kernel's parameter bank and
+// are uniform across the grid, so each `switch` is a uniform branch (ptxas
+// lowers it to a shallow compare tree; a gap-free key layout did not make it
+// emit a BRX jump table); every case touches stack registers with
+// compile-time indices.  LOAD takes its operand index at run time from the
+// source (a shared-memory address under the TMA driver).  One dispatch
+// evaluates UD whole 16-byte units.
 #define COOT_KEY(op, d) ((op) * 9 + (d))
 
 template <int KMAX, int SMAX>
@@ -182,12 +183,16 @@ struct InterpEval {
   case COOT_KEY(COOT_OP_##OP, d):                                          \
     if constexpr ((d) >= 1 && (d) <= SMAX && op_legal<T>(COOT_OP_##OP)) {  \
       un_vec<COOT_OP_##OP>(st[(d) >= 1 ? (d) - 1 : 0]);                    \
+    } else if constexpr ((d) >= 1 && (d) <= SMAX) {                        \
+      __trap(); /* op illegal for T: rejected on the host (R9) */          \
     }                                                                      \
     break;
 #define COOT_BIN_CASE(OP, d)                                               \
   case COOT_KEY(COOT_OP_##OP, d):                                          \
     if constexpr ((d) >= 2 && (d) <= SMAX && op_legal<T>(COOT_OP_##OP)) {  \
       bin_vec<COOT_OP_##OP>(st[(d) >= 2 ? (d) - 2 : 0], st[(d) >= 2 ? (d) - 1 : 0]); \
+    } else if constexpr ((d) >= 2 && (d) <= SMAX) {                        \
+      __trap(); /* op illegal for T: rejected on the host (R9) */          \
     }                                                                      \
     break;
 #define COOT_D(M, ...) M(__VA_ARGS__ 0) M(__VA_ARGS__ 1) M(__VA_ARGS__ 2) M(__VA_ARGS__ 3) \
@@ -403,9 +408,12 @@ constexpr int kTmaThreads = (kConsumerWarps + 1) * 32;
 #define COOT_UD 2
 #endif
 constexpr int kTileUnits = 2 * kConsumerWarps * 32;  // 512 units = 8 KB per operand
-template <class EV>
+// 16-byte units per evaluator dispatch: COOT_UD, except 1 for the 8-operand
+// interpreter and for 8-bit types (16 elements per unit already; their f32
+// stack of 2 units would not fit the register budget).
+template <class T, class EV>
 constexpr int units_per_dispatch() {
-  return (EV::kInterp && EV::K > 4) ? 1 : COOT_UD;
+  return ((EV::kInterp && EV::K > 4) || sizeof(T) == 1) ? 1 : COOT_UD;
 }
 // Resident CTAs per SM the register budget is sized for: 2 (<= 96 registers),
 // except the 8-operand interpreter, which gets the whole register file.
@@ -482,7 +490,7 @@ __global__ void __launch_bounds__(kTmaThreads, tma_min_ctas<EV>())
       const unsigned char* stg = smem + (size_t)s * nk * tile_bytes;
       // each dispatch evaluates UD units (i, i + 256, ...) of the tile together;
       // units are stored / accumulated in increasing order
-      constexpr int UD = units_per_dispatch<EV>();
+      constexpr int UD = units_per_dispatch<T, EV>();
       for (uint32_t i = threadIdx.x; i < nu; i += UD * kConsumerWarps * 32) {
         T v[UD * W];
         EV::template eval_src<T, UD * W>(SmemSrc<T, UD>{stg + (size_t)i * 16, tile_bytes}, a, v);
@@ -595,7 +603,7 @@ __global__ void __launch_bounds__(kTmaThreads, tma_min_ctas<EV>())
   } else {
     T* out = reinterpret_cast<T*>(a.out);
     uint32_t s = 0, ph = 0;
-    constexpr int UD = units_per_dispatch<EV>();
+    constexpr int UD = units_per_dispatch<T, EV>();
     for (u64 p = blockIdx.x; p < npieces; p += gridDim.x) {
       u64 j, r0, len, head, nun;
       piece(p, j, r0, len, head, nun);

@@ -26,8 +26,13 @@ FusedFn driver_kernel(int driver) {
     if (driver == 2) return &fused_strided_kernel<T, ACC, EV>;
     if (driver == 3) return &fused_cols_tma_kernel<T, ACC, EV>;
   }
-  if (driver == 1) return &fused_tma_kernel<T, ACC, EV>;
-  return &fused_kernel<T, ACC, EV, U>;
+  if constexpr (is_narrow<T>()) {
+    // 16/8-bit types: TMA driver only (the host never plans driver 0 for them)
+    return driver == 1 ? &fused_tma_kernel<T, ACC, EV> : nullptr;
+  } else {
+    if (driver == 1) return &fused_tma_kernel<T, ACC, EV>;
+    return &fused_kernel<T, ACC, EV, U>;
+  }
 }
 
 template <class T, int ACC, int... Code>

@@ -548,7 +548,9 @@ coot_status run_fused(coot_ctx* ctx, const coot_expr* e, const Shape& sh, int ac
   }
   const u64 scalar_work = std::max<u64>(a.head, n - a.tail_begin);
   coot::FusedPlan p;
-  p.driver = ctx->driver;
+  // the register-pipelined LDG alternative is built for the 4/8-byte types
+  // only; 16- and 8-bit types always take the TMA driver
+  p.driver = elem_size(e->elem) >= 4 ? ctx->driver : 1;
   p.smem = 0;
   u64 grid;
   if (p.driver == 1) {
