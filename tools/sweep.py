@@ -28,6 +28,9 @@ WL = {
     "c2_reduce": ("f32", 10000, 10000, "L0 L1 MUL EXP S0 L2 MUL ADD", [3.0], "ACCU", False, False),
     "c2_interp": ("f32", 10000, 10000, "L0 L1 MUL EXP S0 L2 MUL ADD", [3.0], "ACCU", True, True),
     "c2_eval": ("f32", 10000, 10000, "L0 L1 MUL EXP S0 L2 MUL ADD", [3.0], None, True, False),
+    "axpy_interp_2p30": ("f32", 1 << 30, 1, "S0 L0 MUL L1 ADD", [2.5], "ACCU", True, True),
+    "poly_interp_2p30": ("f32", 1 << 30, 1, "L0 L1 MUL L2 ADD L0 MUL S0 SUB ABS SQRT", [0.5], "ACCU", True, True),
+    "f64_c2_interp_2p29": ("f64", 1 << 29, 1, "L0 L1 MUL EXP S0 L2 MUL ADD", [3.0], "ACCU", False, True),
     "hl_c2_2p30": ("f32", 1 << 30, 1, "L0 L1 MUL EXP S0 L2 MUL ADD", [3.0], "ACCU", False, False),
     "axpy_accu_2p30": ("f32", 1 << 30, 1, "S0 L0 MUL L1 ADD", [2.5], "ACCU", True, False),
     "axpy_reduce_2p30": ("f32", 1 << 30, 1, "S0 L0 MUL L1 ADD", [2.5], "ACCU", False, False),
