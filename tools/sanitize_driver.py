@@ -68,6 +68,34 @@ def main():
                 torch.cuda.synchronize()
                 ref = oracle.sum_dim("f64", dim, X.cpu().numpy(), m, cols)
                 assert np.allclose(res.cpu().numpy(), ref, rtol=1e-12, atol=0)
+    # 16- and 8-bit element types: fused reductions with Z stored (TMA catalog
+    # and interpreter), statistics / index kinds, dim sums
+    for et in ("bf16", "f16", "e4m3", "e5m2"):
+        tctx = ctxs["tma"]
+        ops = [coot.Mat.randu(n, 1, et, stream=s, ctx=tctx).data for s in range(3)]
+        z = torch.empty(n, dtype=ops[0].dtype, device="cuda")
+        for kind in ("ACCU", "VAR", "INDEX_MAX", "MINMAX", "NORM2"):
+            dt = torch.int64 if kind.startswith("INDEX") else coot.api.RESULT_DTYPE[et]
+            r = torch.zeros(2, dtype=dt, device="cuda")
+            for c in (ctxs["tma"], ctxs["interp"]):
+                c.reduce(et, n, 1, c2, ops, [3.0], kind, r, z)
+        X = coot.Mat.randu(700, 130, et, stream=5, ctx=tctx)
+        for dim in (0, 1):
+            res = torch.zeros(130 if dim == 0 else 700, dtype=coot.api.RESULT_DTYPE[et],
+                              device="cuda")
+            tctx.reduce(et, 700, 130, P("L0"), [X.data], [], f"SUM_DIM{dim}", res)
+        torch.cuda.synchronize()
+        zr = oracle.eval_program(et, c2, [oracle.fill(et, "randu", n, stream=s) for s in range(3)],
+                                 [3.0])
+        zh = z.cpu().view(torch.int16 if z.element_size() == 2 else torch.uint8).numpy()
+        assert np.array_equal(zh.view(zr.dtype), zr), et
+    # views: strided diagonal update and a column-streamed submatrix expression
+    M = coot.Mat.randu(300, 300, "f32", stream=6, ctx=ctxs["tma"])
+    d = M.diag()
+    d += 100.0
+    sub = M.submat(10, 20, 200, 250)
+    sub.assign(2.5 * sub + 1.0, ctx=ctxs["tma"])
+    torch.cuda.synchronize()
     # partial + combine, fill
     ctx = ctxs["tma"]
     parts = torch.zeros(3 * 4, dtype=torch.int64, device="cuda")
