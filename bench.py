@@ -322,6 +322,13 @@ def main():
     # COOT_BENCH_FORCE_DIST=1 (under torchrun) runs the N>1 code path — partial
     # kernel, NCCL all-gather, combine kernel — even with a single rank.
     reducer = cdist.DistReducer(ctx) if (world > 1 or force_dist) else None
+    # N>1: the exchange runs inside the fused kernel over peer memory
+    # (coot_reduce_exchange, mailboxes mapped with CUDA IPC); if any rank cannot
+    # map its peers, or COOT_BENCH_EXCHANGE=nccl, the NCCL all-gather of the
+    # 32-byte partials + combine kernel is used instead
+    exchange = os.environ.get("COOT_BENCH_EXCHANGE", "mailbox")
+    mailbox = (cdist.MailboxExchange.try_create(ctx)
+               if (reducer is not None and exchange == "mailbox") else None)
 
     kern_ev = []
 
@@ -336,6 +343,14 @@ def main():
             res = torch.empty(1, dtype=torch.float32, device=dev)
             ctx.reduce(lw.elem, lw.n_rows, lw.n_cols, lw.program, lw.operands, lw.scalars,
                        "ACCU", res, Z.data)
+            if record:
+                e1 = torch.cuda.Event(enable_timing=True)
+                e1.record(stream)
+                kern_ev.append((e0, e1))
+            return res
+        if mailbox is not None:
+            # a3-a6 in ONE kernel: reduce, publish to the peers' mailboxes, combine
+            res = mailbox.reduce(lw, "ACCU", out=Z.data)
             if record:
                 e1 = torch.cuda.Event(enable_timing=True)
                 e1.record(stream)
@@ -440,6 +455,8 @@ def main():
                "ms_per_step": e_ms}
         del host
 
+    if mailbox is not None:
+        mailbox.close()  # collective: every rank is here
     if rank != 0:
         if world > 1:
             dist.barrier()
@@ -476,6 +493,9 @@ def main():
         "config": {"workload": WORKLOAD, "n_rows": M_ROWS, "n_cols": N_COLS,
                    "global_elements": total_elems, "mode": "eval+accu (Z stored)",
                    "parallelism": f"dp{world} (column blocks)",
+                   "exchange": ("none (one rank)" if reducer is None else
+                                "in-kernel mailboxes (CUDA IPC peer memory)" if mailbox else
+                                "NCCL all_gather of 32-byte partials + combine kernel"),
                    "l2": "inputs 1.2 GB + output 0.4 GB per GPU >> 126 MB L2; no flush needed"},
         "elements_per_s": total_elems / (ms_per_step * 1e-3),
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",

@@ -230,6 +230,39 @@ coot_status coot_partial_bytes(uint32_t kind, uint64_t len, uint64_t* bytes);
 coot_status coot_shard_range(uint64_t n, uint32_t rank, uint32_t nranks, uint64_t align,
                              uint64_t* begin, uint64_t* end);
 
+/* In-kernel exchange (SURVEY §8(e) upgrade path / §8(f) row 4): the fused
+ * reduction kernel itself publishes this rank's partial record to every
+ * peer's MAILBOX over peer memory (NVLink P2P via CUDA IPC), raises a flag,
+ * waits for all nranks flags in its own mailbox and combines the records in
+ * rank order 0..nranks-1 with one rounding — one kernel per rank, no host
+ * round trip, every rank ends with identical bits (same combine as
+ * coot_combine).
+ *
+ * coot_mailbox_create: allocates (cudaMalloc, zeroed) a mailbox for up to
+ *   COOT_MAX_RANKS ranks on the ctx device and writes its CUDA IPC handle
+ *   (COOT_IPC_HANDLE_BYTES bytes, opaque) to `ipc_handle` (host memory).
+ * coot_mailbox_open: maps a PEER process's mailbox from its handle (do not
+ *   open your own: use the pointer create returned).  coot_mailbox_close
+ *   unmaps it; coot_mailbox_destroy frees your own.
+ * coot_reduce_exchange: like coot_reduce over this rank's shard, for the
+ *   scalar kinds (not SUM_DIM*).  `mailboxes` is a HOST array of nranks
+ *   device pointers as mapped in this process (mailboxes[rank] = own).
+ *   `epoch` must be the same on every rank and larger than any epoch used
+ *   before with these mailboxes (e.g. a call counter starting at 1).  Every
+ *   rank must make the matching call; a rank that never arrives makes the
+ *   others time out (~20 s) with a device fault (COOT_ERR_DEVICE on the next
+ *   synchronising call).  MIN/MAX/MINMAX/INDEX of a globally empty
+ *   expression return the identities / ~0. */
+#define COOT_MAX_RANKS 8
+#define COOT_IPC_HANDLE_BYTES 64
+coot_status coot_mailbox_create(coot_ctx* ctx, void** mailbox, void* ipc_handle);
+coot_status coot_mailbox_open(coot_ctx* ctx, const void* ipc_handle, void** peer_mailbox);
+coot_status coot_mailbox_close(coot_ctx* ctx, void* peer_mailbox);
+coot_status coot_mailbox_destroy(coot_ctx* ctx, void* mailbox);
+coot_status coot_reduce_exchange(coot_ctx* ctx, const coot_expr* e, uint32_t kind,
+                                 void* const* mailboxes, uint32_t nranks, uint32_t rank,
+                                 uint64_t epoch, void* result, void* out_or_null);
+
 /* Synthetic inputs (fill::randu, and structured fills for closed
  * forms): out[i] = f(global index start+i) of an operand with n_rows rows,
  * stream = operand index, using the counter-based SplitMix64 recipe of

@@ -98,7 +98,15 @@ _SIGS = {
     "coot_fill": (_i32, [_vp, _u32, _u32, _u64, _u64, _u64, _u64, _u64, _u64, _vp]),
     "coot_sync": (_i32, [_vp]),
     "coot_stats": (_i32, [_vp, ctypes.POINTER(Stats)]),
+    "coot_mailbox_create": (_i32, [_vp, ctypes.POINTER(_vp), _vp]),
+    "coot_mailbox_open": (_i32, [_vp, _vp, ctypes.POINTER(_vp)]),
+    "coot_mailbox_close": (_i32, [_vp, _vp]),
+    "coot_mailbox_destroy": (_i32, [_vp, _vp]),
+    "coot_reduce_exchange": (_i32, [_vp, ctypes.POINTER(Expr), _u32, ctypes.POINTER(_vp), _u32,
+                                    _u32, _u64, _vp, _vp]),
 }
+MAX_RANKS = 8
+IPC_HANDLE_BYTES = 64
 
 
 def _load():

@@ -113,6 +113,36 @@ class Context:
                                ctypes.c_void_p(partials.data_ptr()), nparts, length,
                                ctypes.c_void_p(result.data_ptr())))
 
+    # ---- in-kernel exchange (coot.h "In-kernel exchange") -------------------
+    def mailbox_create(self) -> tuple[int, bytes]:
+        """A zeroed mailbox on this device: (device pointer, CUDA IPC handle)."""
+        p = ctypes.c_void_p()
+        h = ctypes.create_string_buffer(N.IPC_HANDLE_BYTES)
+        check(lib.coot_mailbox_create(self.handle, ctypes.byref(p), h))
+        return int(p.value), h.raw
+
+    def mailbox_open(self, ipc_handle: bytes) -> int:
+        p = ctypes.c_void_p()
+        h = ctypes.create_string_buffer(bytes(ipc_handle), N.IPC_HANDLE_BYTES)
+        check(lib.coot_mailbox_open(self.handle, h, ctypes.byref(p)))
+        return int(p.value)
+
+    def mailbox_close(self, ptr: int):
+        check(lib.coot_mailbox_close(self.handle, ctypes.c_void_p(ptr)))
+
+    def mailbox_destroy(self, ptr: int):
+        check(lib.coot_mailbox_destroy(self.handle, ctypes.c_void_p(ptr)))
+
+    def reduce_exchange(self, elem, n_rows, n_cols, program, operands, scalars, kind,
+                        mailboxes, rank: int, epoch: int, result: torch.Tensor,
+                        out: torch.Tensor | None = None):
+        e = N.make_expr(elem, n_rows, n_cols, program, operands, scalars)
+        mb = (ctypes.c_void_p * len(mailboxes))(*mailboxes)
+        check(lib.coot_reduce_exchange(self.handle, ctypes.byref(e), N.KIND[kind], mb,
+                                       len(mailboxes), rank, epoch,
+                                       ctypes.c_void_p(result.data_ptr()),
+                                       ctypes.c_void_p(out.data_ptr() if out is not None else 0)))
+
     def fill(self, out: torch.Tensor, kind: str = "randu", *, seed: int = 42, stream: int = 0,
              start: int = 0, n_rows: int = 1, k: int = 1):
         check(lib.coot_fill(self.handle, N.ELEM[elem_of(out)], N.FILL[kind], seed, stream, start,

@@ -87,7 +87,15 @@ enum AccKind {
   ACC_NONE = 0, ACC_SUM = 1, ACC_SUMSQ = 2, ACC_MINMAX = 3,
   ACC_VAR = 4, ACC_IMIN = 5, ACC_IMAX = 6
 };
-enum FinalMode { FINAL_ROUND = 0, FINAL_PARTIAL = 1 };
+enum FinalMode { FINAL_ROUND = 0, FINAL_PARTIAL = 1, FINAL_EXCHANGE = 2 };
+
+// In-kernel exchange (FINAL_EXCHANGE): mailbox of rank p at mbox[p] (this
+// process's mapping): records slot[0..P) then u64 flags[0..P).
+struct Exchange {
+  unsigned long long mbox[COOT_MAX_RANKS];
+  unsigned long long epoch;
+  uint32_t nranks, rank;
+};
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
@@ -126,6 +134,7 @@ struct FusedArgs {
   uint32_t nseg;
   uint16_t key[COOT_MAX_INSTR];  // interpreter dispatch index: op * 9 + depth
   uint8_t arg[COOT_MAX_INSTR];
+  Exchange ex;  // FINAL_EXCHANGE only
 };
 
 template <class T>
@@ -1196,6 +1205,81 @@ __device__ __forceinline__ Accum<T, ACC> block_reduce(Accum<T, ACC> acc) {
   return r;
 }
 
+// Merge partial records of consecutive shards in rank order 0..nparts-1 and
+// round once into `result` (index reductions: shard-local index + the element
+// count of the shards before it).  Shared by coot_combine and the exchange.
+template <class T, int ACC, class LoadRec>
+__device__ __forceinline__ void combine_in_order(uint32_t nparts, LoadRec load, uint32_t kind,
+                                                 void* result) {
+  Accum<T, ACC> acc;
+  acc.init();
+  u64 before = 0;
+  for (uint32_t p = 0; p < nparts; ++p) {
+    const Rec r = load(p);
+    Accum<T, ACC> o;
+    o.from_rec(r);
+    if constexpr (ACC == ACC_IMIN || ACC == ACC_IMAX) {
+      if (o.idx != ~0ull) o.idx += before;  // shard-local -> global index
+    }
+    acc.merge(o);
+    before += r.count;
+  }
+  write_final<T, ACC>(acc, kind, result, before);
+}
+
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+// FINAL_EXCHANGE, one thread.  Mailbox layout: records slot[2][MAX_RANKS]
+// (double-buffered by epoch parity), then u64 flag[MAX_RANKS].  Publish this
+// rank's record into slot[epoch & 1][rank] of every peer's mailbox (remote
+// stores over NVLink / peer memory), then raise flag[rank] = epoch there
+// (system-scope release: the record is visible before the flag); wait until
+// every flag of the OWN mailbox reaches epoch (acquire) and combine
+// slot[epoch & 1][0..P) in rank order.  Parity buffering: a fast rank's record
+// for epoch e+1 lands in the other half, and it cannot reach e+2 before this
+// rank has raised its e+1 flags, i.e. finished reading epoch e.  A peer that
+// never arrives -> trap after ~20 s (the host sees a device fault).
+template <class T, int ACC>
+__device__ void exchange_finish(const Rec& mine, const Exchange& ex, uint32_t kind, void* result) {
+  const uint32_t P = ex.nranks;
+  const unsigned long long half = (ex.epoch & 1ull) * COOT_MAX_RANKS;
+  const unsigned long long flag_off = 2ull * COOT_MAX_RANKS * sizeof(Rec);
+  for (uint32_t p = 0; p < P; ++p) {
+    Rec* slot = reinterpret_cast<Rec*>(ex.mbox[p]) + half + ex.rank;
+    __stcg(&slot->a, mine.a);
+    __stcg(&slot->b, mine.b);
+    __stcg(&slot->count, mine.count);
+    __stcg(&slot->pad, 0ull);
+  }
+  __threadfence_system();
+  for (uint32_t p = 0; p < P; ++p)
+    st_release_sys(reinterpret_cast<unsigned long long*>(ex.mbox[p] + flag_off) + ex.rank,
+                   ex.epoch);
+  const unsigned long long* own =
+      reinterpret_cast<const unsigned long long*>(ex.mbox[ex.rank] + flag_off);
+  const unsigned long long t0 = globaltimer_ns();
+  for (uint32_t q = 0; q < P; ++q) {
+    while (ld_acquire_sys(own + q) < ex.epoch) {
+      __nanosleep(256);
+      if (globaltimer_ns() - t0 > 20000000000ull) __trap();  // a rank never arrived
+    }
+  }
+  const Rec* slots = reinterpret_cast<const Rec*>(ex.mbox[ex.rank]) + half;
+  combine_in_order<T, ACC>(P, [&](uint32_t q) { return load_rec_cg(slots + q); }, kind, result);
+}
+
 // Deterministic single-launch finish: every block publishes a record; the
 // last block to arrive (ticket) combines ALL records in block order
 // (lane-strided, then a fixed butterfly) and rounds once.  The ticket
@@ -1203,7 +1287,8 @@ __device__ __forceinline__ Accum<T, ACC> block_reduce(Accum<T, ACC> acc) {
 template <class T, int ACC>
 __device__ __forceinline__ void grid_finish(const Accum<T, ACC>& block_total, Rec* partials,
                                             unsigned* ticket, uint32_t final_mode,
-                                            uint32_t kind, void* result, u64 count) {
+                                            uint32_t kind, void* result, u64 count,
+                                            const Exchange& ex) {
   __shared__ bool am_last;
   if (threadIdx.x == 0) {
     partials[blockIdx.x] = block_total.to_rec(0);
@@ -1224,12 +1309,14 @@ __device__ __forceinline__ void grid_finish(const Accum<T, ACC>& block_total, Re
     }
     acc.warp_reduce();
     if (threadIdx.x == 0) {
+      *ticket = 0u;
       if (final_mode == FINAL_PARTIAL) {
         *reinterpret_cast<Rec*>(result) = acc.to_rec(count);
+      } else if (final_mode == FINAL_EXCHANGE) {
+        exchange_finish<T, ACC>(acc.to_rec(count), ex, kind, result);
       } else {
         write_final<T, ACC>(acc, kind, result, count);
       }
-      *ticket = 0u;
     }
   }
 }

@@ -339,7 +339,7 @@ __global__ void __launch_bounds__(kThreads, EV::kInterp ? 1 : COOT_CAT_MINB)
 
   if constexpr (ACC != ACC_NONE) {
     Accum<T, ACC> bt = block_reduce<T, ACC>(acc);
-    grid_finish<T, ACC>(bt, a.partials, a.ticket, a.final_mode, a.kind, a.result, a.count);
+    grid_finish<T, ACC>(bt, a.partials, a.ticket, a.final_mode, a.kind, a.result, a.count, a.ex);
   }
 }
 
@@ -382,7 +382,7 @@ __global__ void __launch_bounds__(kThreads) fused_strided_kernel(const __grid_co
   }
   if constexpr (ACC != ACC_NONE) {
     Accum<T, ACC> bt = block_reduce<T, ACC>(acc);
-    grid_finish<T, ACC>(bt, a.partials, a.ticket, a.final_mode, a.kind, a.result, a.count);
+    grid_finish<T, ACC>(bt, a.partials, a.ticket, a.final_mode, a.kind, a.result, a.count, a.ex);
   }
 }
 
@@ -528,7 +528,7 @@ __global__ void __launch_bounds__(kTmaThreads, tma_min_ctas<EV>())
 
   if constexpr (ACC != ACC_NONE) {
     Accum<T, ACC> bt = block_reduce<T, ACC>(acc);
-    grid_finish<T, ACC>(bt, a.partials, a.ticket, a.final_mode, a.kind, a.result, a.count);
+    grid_finish<T, ACC>(bt, a.partials, a.ticket, a.final_mode, a.kind, a.result, a.count, a.ex);
   } else {
     __syncthreads();  // the producer stays resident until every staged tile is consumed
   }
@@ -658,7 +658,7 @@ __global__ void __launch_bounds__(kTmaThreads, tma_min_ctas<EV>())
   }
   if constexpr (ACC != ACC_NONE) {
     Accum<T, ACC> bt = block_reduce<T, ACC>(acc);
-    grid_finish<T, ACC>(bt, a.partials, a.ticket, a.final_mode, a.kind, a.result, a.count);
+    grid_finish<T, ACC>(bt, a.partials, a.ticket, a.final_mode, a.kind, a.result, a.count, a.ex);
   } else {
     __syncthreads();  // the producer stays resident until every staged tile is consumed
   }

@@ -8,6 +8,7 @@ namespace coot {
 
 struct FusedArgs;
 struct DimArgs;
+struct Exchange;
 
 struct FusedPlan {
   int catalog;       // >= 0 catalog id, -1 interpreter
@@ -39,8 +40,11 @@ cudaError_t launch_dim_t(const DimPlan& p, const DimArgs& a, cudaStream_t s);
 template <class T>
 cudaError_t launch_combine_t(uint32_t kind, int acc, const void* parts, uint32_t nparts,
                              unsigned long long len, void* result, unsigned grid, cudaStream_t s);
+// identity record of an empty shard into `out`; with ex != nullptr the record
+// is exchanged instead and `out` receives the combined result
 template <class T>
-cudaError_t launch_empty_rec_t(int acc, void* out, cudaStream_t s);
+cudaError_t launch_empty_rec_t(int acc, void* out, cudaStream_t s, const Exchange* ex,
+                               uint32_t kind);
 template <class T>
 cudaError_t launch_fill_t(uint32_t kind, unsigned long long seed, unsigned long long stream,
                           unsigned long long start, unsigned long long count,

@@ -174,19 +174,7 @@ template <class T, int ACC>
 __global__ void combine_rec_kernel(const Rec* parts, uint32_t nparts, uint32_t kind,
                                    void* result) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  Accum<T, ACC> acc;
-  acc.init();
-  u64 before = 0;  // elements of the parts before p: shards are contiguous blocks
-  for (uint32_t p = 0; p < nparts; ++p) {
-    Accum<T, ACC> o;
-    o.from_rec(parts[p]);
-    if constexpr (ACC == ACC_IMIN || ACC == ACC_IMAX) {
-      if (o.idx != ~0ull) o.idx += before;  // shard-local -> global index
-    }
-    acc.merge(o);
-    before += parts[p].count;
-  }
-  write_final<T, ACC>(acc, kind, result, before);
+  combine_in_order<T, ACC>(nparts, [&](uint32_t p) { return parts[p]; }, kind, result);
 }
 
 // Vector partials (SUM_DIM*): result[i] = round(sum_p parts[p][i]), p in order.
@@ -204,12 +192,15 @@ __global__ void combine_vec_kernel(const typename SumT<T>::type* parts, uint32_t
   }
 }
 
-// Identity record for an empty shard (no elements => no kernel to publish it).
+// Identity record for an empty shard (no elements => no kernel to publish it):
+// written to `out`, or (exchange mode) published to the peers' mailboxes and
+// combined into the result `out`.
 template <class T, int ACC>
-__global__ void empty_rec_kernel(Rec* out) {
+__global__ void empty_rec_kernel(Rec* out, const Exchange ex, uint32_t kind, int exchange) {
   Accum<T, ACC> acc;
   acc.init();
-  *out = acc.to_rec(0);
+  if (exchange) exchange_finish<T, ACC>(acc.to_rec(0), ex, kind, out);
+  else *out = acc.to_rec(0);
 }
 
 template <class T>
@@ -249,27 +240,30 @@ cudaError_t launch_combine_t(uint32_t kind, int acc, const void* parts, uint32_t
 }
 
 template <class T>
-cudaError_t launch_empty_rec_t(int acc, void* out, cudaStream_t s) {
+cudaError_t launch_empty_rec_t(int acc, void* out, cudaStream_t s, const Exchange* ex,
+                               uint32_t kind) {
   Rec* r = reinterpret_cast<Rec*>(out);
+  const Exchange e = ex ? *ex : Exchange{};
+  const int x = ex != nullptr;
   switch (acc) {
-    case ACC_SUM: empty_rec_kernel<T, ACC_SUM><<<1, 1, 0, s>>>(r); break;
+    case ACC_SUM: empty_rec_kernel<T, ACC_SUM><<<1, 1, 0, s>>>(r, e, kind, x); break;
     case ACC_SUMSQ:
       if constexpr (is_float<T>()) {
-        empty_rec_kernel<T, ACC_SUMSQ><<<1, 1, 0, s>>>(r);
+        empty_rec_kernel<T, ACC_SUMSQ><<<1, 1, 0, s>>>(r, e, kind, x);
         break;
       } else {
         return cudaErrorInvalidValue;
       }
-    case ACC_MINMAX: empty_rec_kernel<T, ACC_MINMAX><<<1, 1, 0, s>>>(r); break;
+    case ACC_MINMAX: empty_rec_kernel<T, ACC_MINMAX><<<1, 1, 0, s>>>(r, e, kind, x); break;
     case ACC_VAR:
       if constexpr (is_float<T>()) {
-        empty_rec_kernel<T, ACC_VAR><<<1, 1, 0, s>>>(r);
+        empty_rec_kernel<T, ACC_VAR><<<1, 1, 0, s>>>(r, e, kind, x);
         break;
       } else {
         return cudaErrorInvalidValue;
       }
-    case ACC_IMIN: empty_rec_kernel<T, ACC_IMIN><<<1, 1, 0, s>>>(r); break;
-    case ACC_IMAX: empty_rec_kernel<T, ACC_IMAX><<<1, 1, 0, s>>>(r); break;
+    case ACC_IMIN: empty_rec_kernel<T, ACC_IMIN><<<1, 1, 0, s>>>(r, e, kind, x); break;
+    case ACC_IMAX: empty_rec_kernel<T, ACC_IMAX><<<1, 1, 0, s>>>(r, e, kind, x); break;
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();
@@ -345,7 +339,8 @@ cudaError_t launch_fill_t(uint32_t kind, u64 seed, u64 stream, u64 start, u64 co
   template cudaError_t launch_dim_t<T>(const DimPlan&, const DimArgs&, cudaStream_t);         \
   template cudaError_t launch_combine_t<T>(uint32_t, int, const void*, uint32_t, u64, void*,  \
                                            unsigned, cudaStream_t);                           \
-  template cudaError_t launch_empty_rec_t<T>(int, void*, cudaStream_t);                       \
+  template cudaError_t launch_empty_rec_t<T>(int, void*, cudaStream_t, const Exchange*,       \
+                                             uint32_t);                                       \
   template cudaError_t launch_fill_t<T>(uint32_t, u64, u64, u64, u64, u64, u64, void*,        \
                                         unsigned, cudaStream_t);
 

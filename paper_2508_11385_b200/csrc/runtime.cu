@@ -41,6 +41,7 @@ struct coot_ctx {
   size_t dim_tickets_n = 0;
   coot_stats_t stats{};
   bool log = false;
+  const coot::Exchange* pending_ex = nullptr;  // set by coot_reduce_exchange for one call
 };
 
 namespace {
@@ -463,6 +464,7 @@ coot_status run_strided(coot_ctx* ctx, const coot_expr* e, const Shape& sh, int 
   a.count = n;
   a.final_mode = final_mode;
   a.kind = kind;
+  if (final_mode == coot::FINAL_EXCHANGE) a.ex = *ctx->pending_ex;
   coot::FusedPlan p;
   p.driver = 2;
   p.smem = 0;
@@ -576,6 +578,7 @@ coot_status run_fused(coot_ctx* ctx, const coot_expr* e, const Shape& sh, int ac
   a.count = n;
   a.final_mode = final_mode;
   a.kind = kind;
+  if (final_mode == coot::FINAL_EXCHANGE) a.ex = *ctx->pending_ex;
 
   p.catalog = (ctx->flags & COOT_INIT_FORCE_INTERP) ? -1 : match_catalog(e);
   if (acc >= coot::ACC_VAR && p.catalog > 0) p.catalog = -1;  // see pick_fused_acc
@@ -788,17 +791,20 @@ coot_status reduce_common(coot_ctx* ctx, const coot_expr* e, uint32_t kind, void
   if (dim) return run_dim(ctx, &cx, sh, kind, result, final_mode);
   const int acc = acc_for_kind(kind);
   if (n == 0) {
-    if (final_mode == coot::FINAL_PARTIAL) {
+    if (final_mode == coot::FINAL_PARTIAL || final_mode == coot::FINAL_EXCHANGE) {
+      // an empty shard still publishes (or exchanges) the identity record
+      const coot::Exchange* ex = final_mode == coot::FINAL_EXCHANGE ? ctx->pending_ex : nullptr;
+      cudaStream_t s = ctx->stream;
       cudaError_t cerr;
       switch (e->elem) {
-        case COOT_F32: cerr = coot::launch_empty_rec_t<float>(acc, result, ctx->stream); break;
-        case COOT_F64: cerr = coot::launch_empty_rec_t<double>(acc, result, ctx->stream); break;
-        case COOT_U32: cerr = coot::launch_empty_rec_t<uint32_t>(acc, result, ctx->stream); break;
-        case COOT_BF16: cerr = coot::launch_empty_rec_t<coot::bf16>(acc, result, ctx->stream); break;
-        case COOT_F16: cerr = coot::launch_empty_rec_t<coot::f16>(acc, result, ctx->stream); break;
-        case COOT_E4M3: cerr = coot::launch_empty_rec_t<coot::e4m3>(acc, result, ctx->stream); break;
-        case COOT_E5M2: cerr = coot::launch_empty_rec_t<coot::e5m2>(acc, result, ctx->stream); break;
-        default: cerr = coot::launch_empty_rec_t<coot::s64>(acc, result, ctx->stream); break;
+        case COOT_F32: cerr = coot::launch_empty_rec_t<float>(acc, result, s, ex, kind); break;
+        case COOT_F64: cerr = coot::launch_empty_rec_t<double>(acc, result, s, ex, kind); break;
+        case COOT_U32: cerr = coot::launch_empty_rec_t<uint32_t>(acc, result, s, ex, kind); break;
+        case COOT_BF16: cerr = coot::launch_empty_rec_t<coot::bf16>(acc, result, s, ex, kind); break;
+        case COOT_F16: cerr = coot::launch_empty_rec_t<coot::f16>(acc, result, s, ex, kind); break;
+        case COOT_E4M3: cerr = coot::launch_empty_rec_t<coot::e4m3>(acc, result, s, ex, kind); break;
+        case COOT_E5M2: cerr = coot::launch_empty_rec_t<coot::e5m2>(acc, result, s, ex, kind); break;
+        default: cerr = coot::launch_empty_rec_t<coot::s64>(acc, result, s, ex, kind); break;
       }
       if (cerr != cudaSuccess) return cuda_fail(cerr, "empty record launch");
       ctx->stats.launches++;
@@ -957,6 +963,87 @@ coot_status coot_reduce(coot_ctx* ctx, const coot_expr* e, uint32_t kind, void* 
 coot_status coot_reduce_partial(coot_ctx* ctx, const coot_expr* e, uint32_t kind, void* partial,
                                 void* out_or_null) {
   return reduce_common(ctx, e, kind, partial, out_or_null, coot::FINAL_PARTIAL);
+}
+
+// ---- in-kernel exchange (mailboxes over CUDA IPC / NVLink peer memory) ------
+// mailbox = COOT_MAX_RANKS records + COOT_MAX_RANKS u64 flags (zeroed once;
+// flags only grow: each call raises them to its epoch).
+static const size_t kMailboxBytes = 4096;
+
+coot_status coot_mailbox_create(coot_ctx* ctx, void** mailbox, void* ipc_handle) {
+  coot_status st = check_ctx(ctx);
+  if (st != COOT_OK) return st;
+  if (!mailbox || !ipc_handle) return fail(COOT_ERR_CONTRACT, "contract: NULL argument");
+  static_assert(sizeof(cudaIpcMemHandle_t) == COOT_IPC_HANDLE_BYTES, "IPC handle size");
+  st = bind_device(ctx);
+  if (st != COOT_OK) return st;
+  void* p = nullptr;
+  cudaError_t ce = cudaMalloc(&p, kMailboxBytes);
+  if (ce != cudaSuccess) return cuda_fail(ce, "cudaMalloc(mailbox)");
+  ce = cudaMemset(p, 0, kMailboxBytes);
+  if (ce == cudaSuccess) ce = cudaIpcGetMemHandle(reinterpret_cast<cudaIpcMemHandle_t*>(ipc_handle), p);
+  if (ce != cudaSuccess) {
+    cudaFree(p);
+    return cuda_fail(ce, "mailbox setup");
+  }
+  *mailbox = p;
+  return ok();
+}
+
+coot_status coot_mailbox_open(coot_ctx* ctx, const void* ipc_handle, void** peer_mailbox) {
+  coot_status st = check_ctx(ctx);
+  if (st != COOT_OK) return st;
+  if (!peer_mailbox || !ipc_handle) return fail(COOT_ERR_CONTRACT, "contract: NULL argument");
+  st = bind_device(ctx);
+  if (st != COOT_OK) return st;
+  cudaIpcMemHandle_t h;
+  memcpy(&h, ipc_handle, sizeof h);
+  cudaError_t ce = cudaIpcOpenMemHandle(peer_mailbox, h, cudaIpcMemLazyEnablePeerAccess);
+  if (ce != cudaSuccess) return cuda_fail(ce, "cudaIpcOpenMemHandle(mailbox)");
+  return ok();
+}
+
+coot_status coot_mailbox_close(coot_ctx* ctx, void* peer_mailbox) {
+  coot_status st = check_ctx(ctx);
+  if (st != COOT_OK) return st;
+  st = bind_device(ctx);
+  if (st != COOT_OK) return st;
+  cudaError_t ce = cudaIpcCloseMemHandle(peer_mailbox);
+  return ce == cudaSuccess ? ok() : cuda_fail(ce, "cudaIpcCloseMemHandle");
+}
+
+coot_status coot_mailbox_destroy(coot_ctx* ctx, void* mailbox) {
+  coot_status st = check_ctx(ctx);
+  if (st != COOT_OK) return st;
+  st = bind_device(ctx);
+  if (st != COOT_OK) return st;
+  cudaError_t ce = cudaFree(mailbox);
+  return ce == cudaSuccess ? ok() : cuda_fail(ce, "cudaFree(mailbox)");
+}
+
+coot_status coot_reduce_exchange(coot_ctx* ctx, const coot_expr* e, uint32_t kind,
+                                 void* const* mailboxes, uint32_t nranks, uint32_t rank,
+                                 uint64_t epoch, void* result, void* out_or_null) {
+  coot_status st = check_ctx(ctx);
+  if (st != COOT_OK) return st;
+  if (kind == COOT_RED_SUM_DIM0 || kind == COOT_RED_SUM_DIM1)
+    return fail(COOT_ERR_CONTRACT, "contract: the in-kernel exchange covers scalar reductions only");
+  if (!mailboxes || nranks == 0 || nranks > COOT_MAX_RANKS || rank >= nranks)
+    return fail(COOT_ERR_BOUNDS, "bounds: nranks %u / rank %u (max %d ranks)", nranks, rank,
+                COOT_MAX_RANKS);
+  if (epoch == 0) return fail(COOT_ERR_CONTRACT, "contract: epoch must be >= 1");
+  coot::Exchange ex{};
+  for (uint32_t p = 0; p < nranks; ++p) {
+    if (!mailboxes[p]) return fail(COOT_ERR_CONTRACT, "contract: mailbox %u is NULL", p);
+    ex.mbox[p] = reinterpret_cast<unsigned long long>(mailboxes[p]);
+  }
+  ex.epoch = epoch;
+  ex.nranks = nranks;
+  ex.rank = rank;
+  ctx->pending_ex = &ex;
+  st = reduce_common(ctx, e, kind, result, out_or_null, coot::FINAL_EXCHANGE);
+  ctx->pending_ex = nullptr;
+  return st;
 }
 
 coot_status coot_partial_bytes(uint32_t kind, uint64_t len, uint64_t* bytes) {

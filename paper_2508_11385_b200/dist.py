@@ -19,7 +19,8 @@ import torch.distributed as dist
 
 from .api import RESULT_DTYPE, Context, Lowered, partial_bytes, shard_range
 
-__all__ = ["shard_range", "column_block", "allgather_partials", "DistReducer"]
+__all__ = ["shard_range", "column_block", "allgather_partials", "DistReducer",
+           "MailboxExchange"]
 
 
 def column_block(n_cols: int, rank: int, world: int) -> tuple[int, int]:
@@ -97,3 +98,71 @@ class DistReducer:
         self.ctx.reduce(lw.elem, lw.n_rows, lw.n_cols, lw.program, lw.operands, lw.scalars,
                         "SUM_DIM0", res)
         return res
+
+
+class MailboxExchange:
+    """Global scalar reductions with the exchange INSIDE the fused kernel
+    (coot_reduce_exchange; SURVEY §8(e) upgrade path, §8(f) row 4): every rank
+    allocates a mailbox, the CUDA IPC handles are all-gathered once (host
+    objects over the process group), and each reduce is ONE kernel per rank
+    that writes its partial into every peer's mailbox over peer memory
+    (NVLink P2P), waits for all of them and combines in rank order — no host
+    round trip, no collective call per reduction.  Same bits as DistReducer
+    (same records, same rank-order combine)."""
+
+    def __init__(self, ctx: Context, group=None):
+        self.ctx = ctx
+        self.group = group
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        self.mine, handle = ctx.mailbox_create()
+        handles = [None] * self.world
+        dist.all_gather_object(handles, handle, group=group)
+        self.mailboxes, mapped = [], True
+        for r, h in enumerate(handles):
+            if r == self.rank:
+                self.mailboxes.append(self.mine)
+                continue
+            try:
+                self.mailboxes.append(ctx.mailbox_open(h))
+            except Exception:  # e.g. no peer access between these devices
+                self.mailboxes.append(None)
+                mapped = False
+        oks = [None] * self.world
+        dist.all_gather_object(oks, mapped, group=group)
+        self.ok = all(oks)  # usable only if EVERY rank mapped every peer
+        self.epoch = 0
+        # no rank may release its mailbox while a peer could still write into it
+        dist.barrier(group)
+
+    @classmethod
+    def try_create(cls, ctx: Context, group=None):
+        """Collective: a MailboxExchange if every rank could map every peer's
+        mailbox, else None on every rank (the caller then uses DistReducer)."""
+        mx = cls(ctx, group)
+        if mx.ok:
+            return mx
+        mx.close()
+        return None
+
+    def reduce(self, lw: Lowered, kind: str, out: torch.Tensor | None = None) -> torch.Tensor:
+        """Full scalar reduction of this rank's block; the GLOBAL result on every
+        rank.  Every rank must call it the same number of times."""
+        if not self.ok:
+            raise RuntimeError("MailboxExchange: some rank could not map every peer's mailbox")
+        self.epoch += 1
+        dtype = torch.int64 if kind.startswith("INDEX") else RESULT_DTYPE[lw.elem]
+        res = torch.empty(2, dtype=dtype, device=self.ctx.device)
+        self.ctx.reduce_exchange(lw.elem, lw.n_rows, lw.n_cols, lw.program, lw.operands,
+                                 lw.scalars, kind, self.mailboxes, self.rank, self.epoch, res,
+                                 out)
+        return res
+
+    def close(self):
+        torch.cuda.synchronize(self.ctx.device)
+        dist.barrier(self.group)  # every rank's last kernel has finished writing
+        for r, p in enumerate(self.mailboxes):
+            if r != self.rank and p is not None:
+                self.ctx.mailbox_close(p)
+        dist.barrier(self.group)
+        self.ctx.mailbox_destroy(self.mine)
