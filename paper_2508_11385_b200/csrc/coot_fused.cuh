@@ -415,6 +415,13 @@ template <class T, class EV>
 constexpr int units_per_dispatch() {
   return ((EV::kInterp && EV::K > 4) || sizeof(T) == 1) ? 1 : COOT_UD;
 }
+// fused_tma_kernel: the small interpreter on 4-byte types takes 4 units (16
+// elements) per dispatch — halving the per-element cost of its uniform
+// instruction dispatch; the host sizes those tiles at 4 * 256 units.
+template <class T, class EV>
+constexpr int tma_units_per_dispatch() {
+  return (EV::kInterp && EV::K <= 4 && sizeof(T) == 4) ? 4 : units_per_dispatch<T, EV>();
+}
 // Resident CTAs per SM the register budget is sized for: 2 (<= 96 registers),
 // except the 8-operand interpreter, which gets the whole register file.
 template <class EV>
@@ -489,8 +496,9 @@ __global__ void __launch_bounds__(kTmaThreads, tma_min_ctas<EV>())
       mbar_wait(&full[s], ph);
       const unsigned char* stg = smem + (size_t)s * nk * tile_bytes;
       // each dispatch evaluates UD units (i, i + 256, ...) of the tile together;
-      // units are stored / accumulated in increasing order
-      constexpr int UD = units_per_dispatch<T, EV>();
+      // units are stored / accumulated in increasing order (TU >= UD * 256, so
+      // units past nu are read from the stage buffer and discarded)
+      constexpr int UD = tma_units_per_dispatch<T, EV>();
       for (uint32_t i = threadIdx.x; i < nu; i += UD * kConsumerWarps * 32) {
         T v[UD * W];
         EV::template eval_src<T, UD * W>(SmemSrc<T, UD>{stg + (size_t)i * 16, tile_bytes}, a, v);

@@ -554,11 +554,17 @@ coot_status run_fused(coot_ctx* ctx, const coot_expr* e, const Shape& sh, int ac
   // only; 16- and 8-bit types always take the TMA driver
   p.driver = elem_size(e->elem) >= 4 ? ctx->driver : 1;
   p.smem = 0;
+  p.catalog = (ctx->flags & COOT_INIT_FORCE_INTERP) ? -1 : match_catalog(e);
+  if (acc >= coot::ACC_VAR && p.catalog > 0) p.catalog = -1;  // see pick_fused_acc
+  p.interp_large = (e->n_operands > 4 || sh.max_depth > 4) ? 1 : 0;
   u64 grid;
   if (p.driver == 1) {
-    // TMA driver geometry: a function of (n, operands, SM count) only.
+    // TMA driver geometry: a function of (n, operands, SM count, evaluator
+    // class) only.  The small interpreter on 4-byte types evaluates 4 units per
+    // dispatch, so its tiles hold 4 * 256 units (coot::tma_units_per_dispatch).
     const u64 nk = e->n_operands;  // compacted: every operand is referenced
-    const u64 tu = coot::kTileUnits;
+    const bool wide_dispatch = p.catalog < 0 && !p.interp_large && elem_size(e->elem) == 4;
+    const u64 tu = wide_dispatch ? 2 * coot::kTileUnits : coot::kTileUnits;
     const u64 tile_bytes_all = nk * tu * 16;
     const u64 stages = std::max<u64>(2, std::min<u64>(8, (96u << 10) / tile_bytes_all));
     a.tile_units = (uint32_t)tu;
@@ -580,9 +586,6 @@ coot_status run_fused(coot_ctx* ctx, const coot_expr* e, const Shape& sh, int ac
   a.kind = kind;
   if (final_mode == coot::FINAL_EXCHANGE) a.ex = *ctx->pending_ex;
 
-  p.catalog = (ctx->flags & COOT_INIT_FORCE_INTERP) ? -1 : match_catalog(e);
-  if (acc >= coot::ACC_VAR && p.catalog > 0) p.catalog = -1;  // see pick_fused_acc
-  p.interp_large = (e->n_operands > 4 || sh.max_depth > 4) ? 1 : 0;
   p.acc = acc;
   p.grid = (unsigned)grid;
   if (ctx->log)
@@ -607,7 +610,7 @@ coot_status run_dim(coot_ctx* ctx, const coot_expr* e, const Shape& sh, uint32_t
   const u64 W = 16 / es;
   const size_t sbytes = 8;  // f64 / u64 partial words
   const u64 nout = kind == COOT_RED_SUM_DIM0 ? n : m;
-  const size_t obytes = final_mode == coot::FINAL_PARTIAL ? sbytes : es;
+  const size_t obytes = final_mode == coot::FINAL_PARTIAL ? sbytes : result_elem_size(e->elem);
   if (m == 0 || n == 0) {
     if (nout) {
       cudaError_t ce = cudaMemsetAsync(result, 0, nout * obytes, ctx->stream);
