@@ -31,6 +31,8 @@ struct coot_ctx {
   int blocks_per_sm = 8;    // LDG driver / dim kernels: CTAs per SM in the grid
   int driver = 1;           // fused pass: 1 = TMA-staged (default), 0 = LDG
   int tma_ctas_per_sm = 2;  // TMA driver: CTAs per SM in the grid
+  int tma_tile_units = 0;   // TMA driver: units per operand tile override (0 = policy)
+  int tma_smem_kb = 0;      // TMA driver: stage-ring budget override in KB (0 = policy)
   int dim_tma = 0;          // sum(X,dim): TMA-staged kernels when the layout allows
   coot::Rec* recs = nullptr;  // per-block records of the fused pass
   unsigned max_grid = 0;
@@ -560,19 +562,29 @@ coot_status run_fused(coot_ctx* ctx, const coot_expr* e, const Shape& sh, int ac
   u64 grid;
   if (p.driver == 1) {
     // TMA driver geometry: a function of (n, operands, SM count, evaluator
-    // class) only.  The small interpreter on 4-byte types evaluates 4 units per
-    // dispatch, so its tiles hold 4 * 256 units (coot::tma_units_per_dispatch).
+    // class) only.  Policy (tools/tma_tune.py sweeps): 16 KB
+    // tiles per operand (1024 units) for <= 3 operands, else 8 KB; a 64 KB
+    // stage ring (>= 2 stages) — more bytes in flight per CTA measured slower
+    // for read-only streams, bigger bulk copies faster.  The small interpreter
+    // on 4-byte types evaluates 4 units per dispatch, so its tiles hold >= 4 *
+    // 256 units (coot::tma_units_per_dispatch).
     const u64 nk = e->n_operands;  // compacted: every operand is referenced
     const bool wide_dispatch = p.catalog < 0 && !p.interp_large && elem_size(e->elem) == 4;
-    const u64 tu = wide_dispatch ? 2 * coot::kTileUnits : coot::kTileUnits;
+    u64 tu = (nk <= 3 || wide_dispatch) ? 2 * coot::kTileUnits : coot::kTileUnits;
+    if (ctx->tma_tile_units)  // override, still >= what the evaluator's dispatch needs
+      tu = std::max<u64>((u64)ctx->tma_tile_units,
+                         wide_dispatch ? 2 * coot::kTileUnits : coot::kTileUnits);
+    const u64 ring = (u64)(ctx->tma_smem_kb ? ctx->tma_smem_kb : 64) << 10;
     const u64 tile_bytes_all = nk * tu * 16;
-    const u64 stages = std::max<u64>(2, std::min<u64>(8, (96u << 10) / tile_bytes_all));
+    const u64 stages = std::max<u64>(2, std::min<u64>(8, ring / tile_bytes_all));
     a.tile_units = (uint32_t)tu;
     a.stages = (uint32_t)stages;
     p.smem = (unsigned)(stages * tile_bytes_all + 2 * stages * 8);
     const u64 ntiles = ceil_div(a.nunits, tu);
     grid = std::max<u64>(ntiles, ceil_div(scalar_work, coot::kConsumerWarps * 32));
-    grid = std::max<u64>(1, std::min<u64>(grid, (u64)ctx->sm_count * ctx->tma_ctas_per_sm));
+    // a ring too big for two CTAs per SM (> ~113 KB) runs one persistent CTA per SM
+    const u64 per_sm = p.smem > (110u << 10) ? 1 : (u64)ctx->tma_ctas_per_sm;
+    grid = std::max<u64>(1, std::min<u64>(grid, (u64)ctx->sm_count * per_sm));
   } else {
     const u64 work = std::max<u64>(a.nunits, scalar_work);
     grid = std::max<u64>(1, ceil_div(work, coot::kThreads));
@@ -897,6 +909,11 @@ coot_status coot_init(coot_ctx** out, int device, void* cuda_stream, uint32_t fl
   ctx->blocks_per_sm = std::max(1, std::min(32, env_int("COOT_BLOCKS_PER_SM", 8)));
   ctx->driver = env_int("COOT_DRIVER", 1) ? 1 : 0;
   ctx->tma_ctas_per_sm = std::max(1, std::min(4, env_int("COOT_TMA_CTAS", 2)));
+  // TMA ring geometry overrides (tuning; 0 = the default policy of run_fused):
+  // tile = a multiple of 512 units, ring budget in KB per CTA
+  const int tile_env = env_int("COOT_TMA_TILE", 0), kb_env = env_int("COOT_TMA_SMEM_KB", 0);
+  ctx->tma_tile_units = tile_env > 0 ? 512 * std::max(1, std::min(8, tile_env / 512)) : 0;
+  ctx->tma_smem_kb = kb_env > 0 ? std::max(32, std::min(200, kb_env)) : 0;
   // dim sums default to the LDG kernels: measured faster on B200 (c3: dim0
   // 7.25 vs 7.04 TB/s, dim1 7.07 vs 6.74 TB/s)
   ctx->dim_tma = env_int("COOT_DIM_TMA", 0) ? 1 : 0;
