@@ -492,17 +492,21 @@ coot_status run_strided(coot_ctx* ctx, const coot_expr* e, const Shape& sh, int 
   if (cols) {
     const u64 G = (u64)ctx->sm_count * ctx->tma_ctas_per_sm;
     const u64 nk = e->n_operands;
-    const u64 tile_el = (u64)coot::kTileUnits * (16 / es);
+    // ring geometry: the fused-pass policy (16 KB tiles for <= 3 operands, 64 KB ring)
+    u64 tu = nk <= 3 ? 2 * coot::kTileUnits : coot::kTileUnits;
+    if (ctx->tma_tile_units) tu = (u64)ctx->tma_tile_units;
+    const u64 ring = (u64)(ctx->tma_smem_kb ? ctx->tma_smem_kb : 64) << 10;
+    const u64 tile_el = tu * (16 / es);
     u64 S = std::max<u64>(1, ceil_div(8 * G, e->n_cols));
     S = std::min<u64>(S, std::max<u64>(1, m / tile_el));
     const u64 L = ceil_div(ceil_div(m, S), tile_el) * tile_el;
     S = ceil_div(m, L);
-    const u64 stage_bytes = nk * coot::kTileUnits * 16;
-    const u64 stages = std::max<u64>(2, std::min<u64>(8, (96u << 10) / stage_bytes));
+    const u64 stage_bytes = nk * tu * 16;
+    const u64 stages = std::max<u64>(2, std::min<u64>(8, ring / stage_bytes));
     a.ncols = e->n_cols;
     a.seg_len = L;
     a.nseg = (uint32_t)S;
-    a.tile_units = coot::kTileUnits;
+    a.tile_units = (uint32_t)tu;
     a.stages = (uint32_t)stages;
     p.driver = 3;
     p.smem = (unsigned)(stages * stage_bytes + 16 * stages);
