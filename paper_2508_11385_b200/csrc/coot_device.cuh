@@ -1124,6 +1124,21 @@ struct Accum {
   }
 };
 
+// First statement of every kernel launched with programmatic stream
+// serialization (coot_launch.cuh launch_k): wait until the previous grid on
+// the stream has completed and its writes are visible, then let the next
+// kernel's CTAs be scheduled as soon as this grid's have all started.
+__device__ __forceinline__ void pdl_enter() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+__device__ __forceinline__ unsigned atom_add_acq_rel_gpu(unsigned* p, unsigned v) {
+  unsigned old;
+  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+
 // Load a record written by another block of this grid (bypass L1).
 __device__ __forceinline__ Rec load_rec_cg(const Rec* p) {
   Rec r;
@@ -1281,8 +1296,9 @@ __device__ void exchange_finish(const Rec& mine, const Exchange& ex, uint32_t ki
 }
 
 // Deterministic single-launch finish: every block publishes a record; the
-// last block to arrive (ticket) combines ALL records in block order
-// (lane-strided, then a fixed butterfly) and rounds once.  The ticket
+// last block to arrive (ticket) combines ALL records in a fixed order (a
+// function of the grid and block size only: block-strided per thread, then
+// block_reduce's fixed tree) and rounds once.  The ticket
 // self-resets so the next launch on the stream can reuse it.
 template <class T, int ACC>
 __device__ __forceinline__ void grid_finish(const Accum<T, ACC>& block_total, Rec* partials,
@@ -1292,31 +1308,32 @@ __device__ __forceinline__ void grid_finish(const Accum<T, ACC>& block_total, Re
   __shared__ bool am_last;
   if (threadIdx.x == 0) {
     partials[blockIdx.x] = block_total.to_rec(0);
-    __threadfence();
-    const unsigned t = atomicAdd(ticket, 1u);
+    // acq_rel: releases this block's record, and (for the last arrival)
+    // acquires every other block's — no separate membar.gl on either side
+    const unsigned t = atom_add_acq_rel_gpu(ticket, 1u);
     am_last = (t == gridDim.x - 1);
   }
-  __syncthreads();
+  __syncthreads();  // extends thread 0's acquire to the whole block
   if (!am_last) return;
-  __threadfence();
-  if (threadIdx.x < 32) {
-    Accum<T, ACC> acc;
-    acc.init();
-    for (unsigned b = threadIdx.x; b < gridDim.x; b += 32) {
-      Accum<T, ACC> o;
-      o.from_rec(load_rec_cg(&partials[b]));
-      acc.merge(o);
-    }
-    acc.warp_reduce();
-    if (threadIdx.x == 0) {
-      *ticket = 0u;
-      if (final_mode == FINAL_PARTIAL) {
-        *reinterpret_cast<Rec*>(result) = acc.to_rec(count);
-      } else if (final_mode == FINAL_EXCHANGE) {
-        exchange_finish<T, ACC>(acc.to_rec(count), ex, kind, result);
-      } else {
-        write_final<T, ACC>(acc, kind, result, count);
-      }
+  // the last block loads the records with all its threads (one L2 round trip
+  // for grids <= blockDim), then reduces them in a fixed tree: thread t merges
+  // records t, t + blockDim, ... in order, then block_reduce
+  Accum<T, ACC> acc;
+  acc.init();
+  for (unsigned b = threadIdx.x; b < gridDim.x; b += blockDim.x) {
+    Accum<T, ACC> o;
+    o.from_rec(load_rec_cg(&partials[b]));
+    acc.merge(o);
+  }
+  const Accum<T, ACC> tot = block_reduce<T, ACC>(acc);
+  if (threadIdx.x == 0) {
+    *ticket = 0u;
+    if (final_mode == FINAL_PARTIAL) {
+      *reinterpret_cast<Rec*>(result) = tot.to_rec(count);
+    } else if (final_mode == FINAL_EXCHANGE) {
+      exchange_finish<T, ACC>(tot.to_rec(count), ex, kind, result);
+    } else {
+      write_final<T, ACC>(tot, kind, result, count);
     }
   }
 }

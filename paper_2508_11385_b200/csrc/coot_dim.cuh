@@ -50,6 +50,7 @@ __device__ __forceinline__ void store_dim_value(const DimArgs& d, u64 idx,
 // ---- K4a: block per (column, segment) — tall columns ------------------------
 template <class T, class EV>
 __global__ void __launch_bounds__(kThreads) dim0_block_kernel(const __grid_constant__ DimArgs d) {
+  pdl_enter();
   constexpr int W = Unit<T>::W;
   constexpr int K = EV::K;
   typedef typename SumT<T>::type S;
@@ -130,6 +131,7 @@ __global__ void __launch_bounds__(kThreads) dim0_block_kernel(const __grid_const
 // ---- K4b: warp per column — short columns (m < 2048) ------------------------
 template <class T, class EV>
 __global__ void __launch_bounds__(kThreads) dim0_warp_kernel(const __grid_constant__ DimArgs d) {
+  pdl_enter();
   constexpr int K = EV::K;
   const int lane = threadIdx.x & 31;
   const u64 warp = ((u64)blockIdx.x * kThreads + threadIdx.x) >> 5;
@@ -165,6 +167,7 @@ __device__ __forceinline__ void load_elem_strided(const FusedArgs& a, u64 i, u64
 
 template <class T, class EV>
 __global__ void __launch_bounds__(kThreads) dim_strided_kernel(const __grid_constant__ DimArgs d) {
+  pdl_enter();
   if (d.dim == 0) {
     const int lane = threadIdx.x & 31;
     const u64 warp = ((u64)blockIdx.x * kThreads + threadIdx.x) >> 5;
@@ -206,6 +209,7 @@ __global__ void __launch_bounds__(kThreads) dim_strided_kernel(const __grid_cons
 // block of the row tile.
 template <class T, class EV>
 __global__ void __launch_bounds__(kThreads) dim1_kernel(const __grid_constant__ DimArgs d) {
+  pdl_enter();
   constexpr int W = Unit<T>::W;
   constexpr int K = EV::K;
   typedef typename SumT<T>::type S;

@@ -273,6 +273,7 @@ __device__ __forceinline__ void load_elem(const FusedArgs& a, u64 e, T (&in)[EV:
 template <class T, int ACC, class EV, int U>
 __global__ void __launch_bounds__(kThreads, EV::kInterp ? 1 : COOT_CAT_MINB)
     fused_kernel(const __grid_constant__ FusedArgs a) {
+  pdl_enter();
   constexpr int W = Unit<T>::W;
   constexpr int K = EV::K;
   Accum<T, ACC> acc;
@@ -352,6 +353,7 @@ __global__ void __launch_bounds__(kThreads, EV::kInterp ? 1 : COOT_CAT_MINB)
 // catalog matching.
 template <class T, int ACC, class EV>
 __global__ void __launch_bounds__(kThreads) fused_strided_kernel(const __grid_constant__ FusedArgs a) {
+  pdl_enter();
   constexpr int K = EV::K;
   Accum<T, ACC> acc;
   acc.init();
@@ -432,6 +434,7 @@ constexpr int tma_min_ctas() {
 template <class T, int ACC, class EV>
 __global__ void __launch_bounds__(kTmaThreads, tma_min_ctas<EV>())
     fused_tma_kernel(const __grid_constant__ FusedArgs a) {
+  pdl_enter();
   constexpr int W = Unit<T>::W;
   constexpr int K = EV::K;
   extern __shared__ __align__(128) unsigned char smem[];
@@ -553,6 +556,7 @@ __global__ void __launch_bounds__(kTmaThreads, tma_min_ctas<EV>())
 template <class T, int ACC, class EV>
 __global__ void __launch_bounds__(kTmaThreads, tma_min_ctas<EV>())
     fused_cols_tma_kernel(const __grid_constant__ FusedArgs a) {
+  pdl_enter();
   constexpr int W = Unit<T>::W;
   constexpr int K = EV::K;
   extern __shared__ __align__(128) unsigned char smem[];

@@ -17,6 +17,7 @@ struct FusedPlan {
   unsigned grid;
   int driver;        // 0 = register-pipelined LDG driver, 1 = TMA-staged driver
   unsigned smem;     // dynamic shared memory (TMA driver)
+  int pdl = 1;       // launch as a programmatic dependent of the previous kernel
 };
 
 enum DimKernel {
@@ -31,6 +32,7 @@ struct DimPlan {
   int interp_large;
   unsigned grid;
   unsigned smem;     // dynamic shared memory (TMA kernels)
+  int pdl = 1;       // launch as a programmatic dependent of the previous kernel
 };
 
 template <class T>

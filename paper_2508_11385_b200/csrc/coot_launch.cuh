@@ -98,6 +98,32 @@ inline cudaError_t allow_smem(const void* fn, unsigned bytes) {
   return e;
 }
 
+// Programmatic dependent launch: the kernel may be scheduled while the previous
+// kernel on the stream is still running (once all of that grid's CTAs have
+// executed griddepcontrol.launch_dependents); every kernel launched this way
+// begins with pdl_enter(), whose griddepcontrol.wait blocks until the previous
+// grid has completed and its memory is visible — so only the launch latency
+// overlaps, never the data.
+template <class Args>
+cudaError_t launch_k(void (*k)(const Args), unsigned grid, unsigned block, unsigned smem,
+                     cudaStream_t s, const Args& a, int pdl) {
+  if (!pdl) {
+    k<<<grid, block, smem, s>>>(a);
+    return cudaGetLastError();
+  }
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k, a);
+}
+
 template <class T>
 cudaError_t launch_fused_t(const FusedPlan& p, const FusedArgs& a, cudaStream_t s) {
   FusedFn k = pick_fused<T>(p);
@@ -105,11 +131,9 @@ cudaError_t launch_fused_t(const FusedPlan& p, const FusedArgs& a, cudaStream_t 
   if (p.driver == 1 || p.driver == 3) {
     cudaError_t e = allow_smem(reinterpret_cast<const void*>(k), p.smem);
     if (e != cudaSuccess) return e;
-    k<<<p.grid, kTmaThreads, p.smem, s>>>(a);
-  } else {
-    k<<<p.grid, kThreads, 0, s>>>(a);
+    return launch_k(k, p.grid, kTmaThreads, p.smem, s, a, p.pdl);
   }
-  return cudaGetLastError();
+  return launch_k(k, p.grid, kThreads, 0, s, a, p.pdl);
 }
 
 // Dimension sums: catalog [L0] (plain matrix) or the interpreter.
@@ -161,11 +185,9 @@ cudaError_t launch_dim_t(const DimPlan& p, const DimArgs& a, cudaStream_t s) {
   if (tma) {
     cudaError_t e = allow_smem(reinterpret_cast<const void*>(k), p.smem);
     if (e != cudaSuccess) return e;
-    k<<<p.grid, kTmaThreads, p.smem, s>>>(a);
-  } else {
-    k<<<p.grid, kThreads, 0, s>>>(a);
+    return launch_k(k, p.grid, kTmaThreads, p.smem, s, a, p.pdl);
   }
-  return cudaGetLastError();
+  return launch_k(k, p.grid, kThreads, 0, s, a, p.pdl);
 }
 
 // ---- multi-GPU combine (K6) and partial bookkeeping -------------------------

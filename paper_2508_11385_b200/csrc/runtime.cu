@@ -34,6 +34,7 @@ struct coot_ctx {
   int tma_tile_units = 0;   // TMA driver: units per operand tile override (0 = policy)
   int tma_smem_kb = 0;      // TMA driver: stage-ring budget override in KB (0 = policy)
   int dim_tma = 0;          // sum(X,dim): TMA-staged kernels when the layout allows
+  int pdl = 1;              // programmatic dependent launch of fused / dim kernels
   coot::Rec* recs = nullptr;  // per-block records of the fused pass
   unsigned max_grid = 0;
   unsigned* ticket = nullptr;  // fused-pass arrival counter
@@ -468,6 +469,7 @@ coot_status run_strided(coot_ctx* ctx, const coot_expr* e, const Shape& sh, int 
   a.kind = kind;
   if (final_mode == coot::FINAL_EXCHANGE) a.ex = *ctx->pending_ex;
   coot::FusedPlan p;
+  p.pdl = ctx->pdl;
   p.driver = 2;
   p.smem = 0;
   p.catalog = -1;
@@ -556,6 +558,7 @@ coot_status run_fused(coot_ctx* ctx, const coot_expr* e, const Shape& sh, int ac
   }
   const u64 scalar_work = std::max<u64>(a.head, n - a.tail_begin);
   coot::FusedPlan p;
+  p.pdl = ctx->pdl;
   // the register-pipelined LDG alternative is built for the 4/8-byte types
   // only; 16- and 8-bit types always take the TMA driver
   p.driver = elem_size(e->elem) >= 4 ? ctx->driver : 1;
@@ -648,6 +651,7 @@ coot_status run_dim(coot_ctx* ctx, const coot_expr* e, const Shape& sh, uint32_t
   const bool col_aligned = ((m * es) % 16) == 0;
   const u64 target = (u64)ctx->sm_count * ctx->blocks_per_sm;
   coot::DimPlan p;
+  p.pdl = ctx->pdl;
   p.catalog = ((ctx->flags & COOT_INIT_FORCE_INTERP) == 0 && e->n_instr == 1) ? 0 : -1;
   p.interp_large = (e->n_operands > 4 || sh.max_depth > 4) ? 1 : 0;
   p.smem = 0;
@@ -925,6 +929,9 @@ coot_status coot_init(coot_ctx** out, int device, void* cuda_stream, uint32_t fl
   // dim sums default to the LDG kernels: measured faster on B200 (c3: dim0
   // 7.25 vs 7.04 TB/s, dim1 7.07 vs 6.74 TB/s)
   ctx->dim_tma = env_int("COOT_DIM_TMA", 0) ? 1 : 0;
+  // back-to-back calls overlap each launch with the previous kernel's tail
+  // (COOT_PDL=0: plain stream-ordered launches)
+  ctx->pdl = env_int("COOT_PDL", 1) ? 1 : 0;
   ctx->max_grid = (unsigned)ctx->sm_count * 32u;
   e = cudaMalloc(&ctx->recs, sizeof(coot::Rec) * ctx->max_grid);
   if (e == cudaSuccess) e = cudaMalloc(&ctx->ticket, 64 * sizeof(unsigned));

@@ -1,6 +1,6 @@
 """Run a few launches of one workload's fused kernel (for ncu captures).
 
-usage: python tools/profile_step.py [c2|c2ro|axpy|c3d0|c3d1|c4u|c4s|dot|norm2] [reps]
+usage: python tools/profile_step.py [c1|c2|c2ro|axpy|c3d0|c3d1|c4u|c4s|dot|norm2] [reps]
 """
 import os
 import sys
@@ -17,6 +17,7 @@ P = lambda s: [(t, 0) if not (t[0] in "LS" and t[1:].isdigit()) else  # noqa: E7
 WL = {
     "c2": ("f32", 10000, 10000, "L0 L1 MUL EXP S0 L2 MUL ADD", [3.0], "ACCU", True),
     "c2ro": ("f32", 10000, 10000, "L0 L1 MUL EXP S0 L2 MUL ADD", [3.0], "ACCU", False),
+    "c1": ("f32", 1_000_000, 1, "S0 L0 MUL L1 ADD", [2.5], "ACCU", True),
     "axpy": ("f32", 1 << 30, 1, "S0 L0 MUL L1 ADD", [2.5], "ACCU", True),
     "c3d0": ("f64", 32768, 32768, "L0", [], "SUM_DIM0", False),
     "c3d1": ("f64", 32768, 32768, "L0", [], "SUM_DIM1", False),

@@ -55,6 +55,33 @@ def per_call_us(ctx, n, reps=100):
     return e0.elapsed_time(e1) / reps * 1e3, ctx.stats()["last_grid"]
 
 
+def torch_us(n, reps=100):
+    """floor reference: torch's own axpy + sum kernels (two launches) on the same n"""
+    x = torch.rand(n, device="cuda")
+    y = torch.rand(n, device="cuda")
+    r = torch.empty((), device="cuda")
+    s = torch.cuda.Stream()
+    out = {}
+    for name, fn in (("torch_axpy", lambda: y.add_(x, alpha=2.5)),
+                     ("torch_sum", lambda: r.copy_(torch.sum(y))),
+                     ("torch_copy", lambda: y.copy_(x))):
+        fn()
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            for _ in range(reps):
+                fn()
+        g.replay()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        g.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        out[name] = e0.elapsed_time(e1) / reps * 1e3
+    return out
+
+
 def main():
     ctxs = {"tma": mkctx(), "tma1cta": mkctx(COOT_TMA_CTAS=1), "ldg": mkctx(COOT_DRIVER=0),
             "ldg4": mkctx(COOT_DRIVER=0, COOT_BLOCKS_PER_SM=4)}
@@ -63,6 +90,8 @@ def main():
         for name, ctx in ctxs.items():
             us, grid = per_call_us(ctx, n)
             row.append(f"{name}={us:7.2f}us(g{grid})")
+        t = torch_us(n)
+        row += [f"{k}={v:7.2f}us" for k, v in t.items()]
         print(f"n={n:>10d} " + " ".join(row), flush=True)
 
 
