@@ -47,6 +47,21 @@ __device__ __forceinline__ void store_dim_value(const DimArgs& d, u64 idx,
   }
 }
 
+// sum(X, dim) never stores element values.  For the plain-matrix program on
+// E4M3 the f32 round trip of a value (exact decode, saturating re-encode, R25)
+// is the identity except for the sign of a NaN, which a sum propagates as NaN
+// either way — so the raw bytes go straight to the accumulation.  (Not E5M2:
+// its +-inf saturate to +-57344 on re-encoding.)
+template <class T, class EV, int W, class In>
+__device__ __forceinline__ void dim_eval(const In& in, const FusedArgs& f, T (&v)[W]) {
+  if constexpr (EV::kIdentity && std::is_same<T, e4m3>::value) {
+#pragma unroll
+    for (int w = 0; w < W; ++w) v[w] = in[0][w];
+  } else {
+    EV::template eval<T, W>(in, f, v);
+  }
+}
+
 // ---- K4a: block per (column, segment) — tall columns ------------------------
 template <class T, class EV>
 __global__ void __launch_bounds__(kThreads) dim0_block_kernel(const __grid_constant__ DimArgs d) {
@@ -73,7 +88,7 @@ __global__ void __launch_bounds__(kThreads) dim0_block_kernel(const __grid_const
     for (u64 i = threadIdx.x; i < head; i += kThreads) {
       T in[K][1], v[1];
       load_elem<T, EV>(d.f, e0 + i, in);
-      EV::template eval<T, 1>(in, d.f, v);
+      dim_eval<T, EV, 1>(in, d.f, v);
       acc.template add<1>(v);
     }
     u64 u = threadIdx.x;
@@ -87,7 +102,7 @@ __global__ void __launch_bounds__(kThreads) dim0_block_kernel(const __grid_const
 #pragma unroll
         for (int q = 0; q < UL; ++q) {
           T v[W];
-          EV::template eval<T, W>(in[q], d.f, v);
+          dim_eval<T, EV, W>(in[q], d.f, v);
           acc.template add<W>(v);
         }
       }
@@ -95,13 +110,13 @@ __global__ void __launch_bounds__(kThreads) dim0_block_kernel(const __grid_const
     for (; u < nun; u += kThreads) {
       T in[K][W], v[W];
       load_units<T, EV>(d.f, e0 + head + u * W, in);
-      EV::template eval<T, W>(in, d.f, v);
+      dim_eval<T, EV, W>(in, d.f, v);
       acc.template add<W>(v);
     }
     for (u64 i = tb + threadIdx.x; i < len; i += kThreads) {
       T in[K][1], v[1];
       load_elem<T, EV>(d.f, e0 + i, in);
-      EV::template eval<T, 1>(in, d.f, v);
+      dim_eval<T, EV, 1>(in, d.f, v);
       acc.template add<1>(v);
     }
     Accum<T, ACC_SUM> bt = block_reduce<T, ACC_SUM>(acc);
@@ -143,7 +158,7 @@ __global__ void __launch_bounds__(kThreads) dim0_warp_kernel(const __grid_consta
     for (u64 i = lane; i < d.m; i += 32) {
       T in[K][1], v[1];
       load_elem<T, EV>(d.f, e0 + i, in);
-      EV::template eval<T, 1>(in, d.f, v);
+      dim_eval<T, EV, 1>(in, d.f, v);
       acc.template add<1>(v);
     }
     acc.warp_reduce();
@@ -178,7 +193,7 @@ __global__ void __launch_bounds__(kThreads) dim_strided_kernel(const __grid_cons
       for (u64 i = lane; i < d.m; i += 32) {
         T in[EV::K][1], v[1];
         load_elem_strided<T, EV>(d.f, i, j, in);
-        EV::template eval<T, 1>(in, d.f, v);
+        dim_eval<T, EV, 1>(in, d.f, v);
         acc.template add<1>(v);
       }
       acc.warp_reduce();
@@ -192,7 +207,7 @@ __global__ void __launch_bounds__(kThreads) dim_strided_kernel(const __grid_cons
       for (u64 j = 0; j < d.n; ++j) {
         T in[EV::K][1], v[1];
         load_elem_strided<T, EV>(d.f, i, j, in);
-        EV::template eval<T, 1>(in, d.f, v);
+        dim_eval<T, EV, 1>(in, d.f, v);
         acc.template add<1>(v);
       }
       store_dim_value<T>(d, i, acc.s);
@@ -239,30 +254,44 @@ __global__ void __launch_bounds__(kThreads) dim1_kernel(const __grid_constant__ 
 #pragma unroll
         for (int c = 0; c < 4; ++c) load_units<T, EV>(d.f, (j + c * G) * d.m + rbase, in[c]);
 #pragma unroll
-        for (int c = 0; c < 4; ++c) EV::template eval<T, W>(in[c], d.f, v[c]);
+        for (int c = 0; c < 4; ++c) dim_eval<T, EV, W>(in[c], d.f, v[c]);
       } else {
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
           T in[K][W];
           load_units<T, EV>(d.f, (j + c * G) * d.m + rbase, in);
-          EV::template eval<T, W>(in, d.f, v[c]);
+          dim_eval<T, EV, W>(in, d.f, v[c]);
         }
       }
+      if constexpr (is_narrow<T>()) {
+        // widen each column's unit on its own (adjacent-byte pairs decode
+        // without repacking), then the same f32 pairwise sum of the 4 columns
+        // as unit_sum<T, 4> — bit-identical to it
+        float x[4][W];
 #pragma unroll
-      for (int w = 0; w < W; ++w) {
-        T col4[4] = {v[0][w], v[1][w], v[2][w], v[3][w]};
-        if constexpr (is_float<T>()) {
-          acc[w] = sum_add<S>(acc[w], unit_sum<T, 4>(col4));
-        } else {
+        for (int c = 0; c < 4; ++c) widen_f32<T, W>(v[c], x[c]);
 #pragma unroll
-          for (int c = 0; c < 4; ++c) acc[w] = sum_add<S>(acc[w], (S)col4[c]);
+        for (int w = 0; w < W; ++w) {
+          const float c4[4] = {x[0][w], x[1][w], x[2][w], x[3][w]};
+          acc[w] = sum_add<S>(acc[w], (S)pairwise_f32<4>(c4));
+        }
+      } else {
+#pragma unroll
+        for (int w = 0; w < W; ++w) {
+          T col4[4] = {v[0][w], v[1][w], v[2][w], v[3][w]};
+          if constexpr (is_float<T>()) {
+            acc[w] = sum_add<S>(acc[w], unit_sum<T, 4>(col4));
+          } else {
+#pragma unroll
+            for (int c = 0; c < 4; ++c) acc[w] = sum_add<S>(acc[w], (S)col4[c]);
+          }
         }
       }
     }
     for (; j < c1; j += G) {
       T in[K][W], v[W];
       load_units<T, EV>(d.f, j * d.m + rbase, in);
-      EV::template eval<T, W>(in, d.f, v);
+      dim_eval<T, EV, W>(in, d.f, v);
 #pragma unroll
       for (int w = 0; w < W; ++w) {
         T one[1] = {v[w]};
@@ -277,7 +306,7 @@ __global__ void __launch_bounds__(kThreads) dim1_kernel(const __grid_constant__ 
         for (u64 j = c0 + g; j < c1; j += G) {
           T in[K][1], v[1];
           load_elem<T, EV>(d.f, j * d.m + r, in);
-          EV::template eval<T, 1>(in, d.f, v);
+          dim_eval<T, EV, 1>(in, d.f, v);
           acc[w] = sum_add<S>(acc[w], unit_sum<T, 1>(v));
         }
       }

@@ -135,6 +135,8 @@ template <int... Code>
 struct CatalogEval<StaticProg<Code...>> {
   static constexpr int K = StaticProg<Code...>::n_ops();
   static constexpr bool kInterp = false;
+  // the program is the plain matrix [L0]
+  static constexpr bool kIdentity = sizeof...(Code) == 1 && StaticProg<Code...>::codes[0] == 0;
   template <class T, int W, class Src>
   __device__ __forceinline__ static void eval_src(const Src& src, const FusedArgs& a, T (&out)[W]) {
     typename ComputeT<T>::type st[COOT_MAX_STACK][W];
@@ -162,6 +164,7 @@ template <int KMAX, int SMAX>
 struct InterpEval {
   static constexpr int K = KMAX;
   static constexpr bool kInterp = true;
+  static constexpr bool kIdentity = false;
 
   template <class T, int W, class Src>
   __device__ __forceinline__ static void eval_src(const Src& src, const FusedArgs& a, T (&out)[W]) {

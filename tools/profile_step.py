@@ -18,6 +18,10 @@ WL = {
     "c2": ("f32", 10000, 10000, "L0 L1 MUL EXP S0 L2 MUL ADD", [3.0], "ACCU", True),
     "c2ro": ("f32", 10000, 10000, "L0 L1 MUL EXP S0 L2 MUL ADD", [3.0], "ACCU", False),
     "c1": ("f32", 1_000_000, 1, "S0 L0 MUL L1 ADD", [2.5], "ACCU", True),
+    "c2ro_bf16": ("bf16", 1 << 15, 1 << 15, "L0 L1 MUL EXP S0 L2 MUL ADD", [3.0], "ACCU", False),
+    "c2ro_e4m3": ("e4m3", 1 << 15, 1 << 16, "L0 L1 MUL EXP S0 L2 MUL ADD", [3.0], "ACCU", False),
+    "c3d1_e4m3": ("e4m3", 65536, 32768, "L0", [], "SUM_DIM1", False),
+    "c3d1_bf16": ("bf16", 32768, 32768, "L0", [], "SUM_DIM1", False),
     "axpy": ("f32", 1 << 30, 1, "S0 L0 MUL L1 ADD", [2.5], "ACCU", True),
     "c3d0": ("f64", 32768, 32768, "L0", [], "SUM_DIM0", False),
     "c3d1": ("f64", 32768, 32768, "L0", [], "SUM_DIM1", False),
@@ -38,7 +42,7 @@ for s, t in enumerate(ops):
     ctx.fill(t, "randu", stream=s, n_rows=m)
 out = torch.empty(m * n, dtype=api.TORCH_DTYPE[elem], device="cuda") if store else None
 rlen = n if kind == "SUM_DIM0" else (m if kind == "SUM_DIM1" else 2)
-res = torch.empty(rlen, dtype=api.TORCH_DTYPE[elem], device="cuda")
+res = torch.empty(rlen, dtype=api.RESULT_DTYPE[elem], device="cuda")
 torch.cuda.synchronize()
 for _ in range(reps):
     ctx.reduce(elem, m, n, prog, ops, sc, kind, res, out)
