@@ -132,8 +132,9 @@ struct FusedArgs {
   // column-segmented view path: pieces = (column, segment of seg_len rows)
   u64 ncols, seg_len;
   uint32_t nseg;
-  uint16_t key[COOT_MAX_INSTR];  // interpreter dispatch index: op * 9 + depth
-  uint8_t arg[COOT_MAX_INSTR];
+  // interpreter instruction: dispatch index (op * 9 + depth) | argument << 16
+  // (one 32-bit word: the constant-bank load lands in a register as is)
+  uint32_t code[COOT_MAX_INSTR];
   Exchange ex;  // FINAL_EXCHANGE only
 };
 

@@ -173,12 +173,12 @@ struct InterpEval {
 
 #define COOT_LOAD_CASE(d)                                                  \
   case COOT_KEY(COOT_OP_LOAD, d):                                          \
-    if constexpr ((d) < SMAX) load_to<T, W>(src, (int)a.arg[i], st[(d) < SMAX ? (d) : 0]); \
+    if constexpr ((d) < SMAX) load_to<T, W>(src, (int)arg, st[(d) < SMAX ? (d) : 0]); \
     break;
 #define COOT_SCALAR_CASE(d)                                                \
   case COOT_KEY(COOT_OP_SCALAR, d):                                        \
     if constexpr ((d) < SMAX) {                                            \
-      const CT s = scalar_as<CT>(a.scalars[a.arg[i]]);                     \
+      const CT s = scalar_as<CT>(a.scalars[arg]);                          \
       _Pragma("unroll") for (int w = 0; w < W; ++w) st[d][w] = s;          \
     }                                                                      \
     break;
@@ -201,9 +201,14 @@ struct InterpEval {
 #define COOT_D(M, ...) M(__VA_ARGS__ 0) M(__VA_ARGS__ 1) M(__VA_ARGS__ 2) M(__VA_ARGS__ 3) \
   M(__VA_ARGS__ 4) M(__VA_ARGS__ 5) M(__VA_ARGS__ 6) M(__VA_ARGS__ 7) M(__VA_ARGS__ 8)
 
+    // the next instruction is fetched before this one is dispatched, so its
+    // constant-bank latency overlaps the case body
+    uint32_t next = a.code[0];
 #pragma unroll 1
     for (uint32_t i = 0; i < a.n_instr; ++i) {
-      switch (a.key[i]) {
+      const uint32_t key = next & 0xffffu, arg = next >> 16;
+      next = a.code[i + 1 < COOT_MAX_INSTR ? i + 1 : i];
+      switch (key) {
         COOT_D(COOT_LOAD_CASE)
         COOT_D(COOT_SCALAR_CASE)
         COOT_D(COOT_UN_CASE, NEG,)
@@ -420,18 +425,24 @@ template <class T, class EV>
 constexpr int units_per_dispatch() {
   return ((EV::kInterp && EV::K > 4) || sizeof(T) == 1) ? 1 : COOT_UD;
 }
+#ifndef COOT_INTERP4_MINB
+#define COOT_INTERP4_MINB 2
+#endif
+#ifndef COOT_INTERP4_UD
+#define COOT_INTERP4_UD 4
+#endif
 // fused_tma_kernel: the small interpreter on 4-byte types takes 4 units (16
 // elements) per dispatch — halving the per-element cost of its uniform
 // instruction dispatch; the host sizes those tiles at 4 * 256 units.
 template <class T, class EV>
 constexpr int tma_units_per_dispatch() {
-  return (EV::kInterp && EV::K <= 4 && sizeof(T) == 4) ? 4 : units_per_dispatch<T, EV>();
+  return (EV::kInterp && EV::K <= 4 && sizeof(T) == 4) ? COOT_INTERP4_UD : units_per_dispatch<T, EV>();
 }
 // Resident CTAs per SM the register budget is sized for: 2 (<= 96 registers),
 // except the 8-operand interpreter, which gets the whole register file.
 template <class EV>
 constexpr int tma_min_ctas() {
-  return (EV::kInterp && EV::K > 4) ? 1 : 2;
+  return (EV::kInterp && EV::K > 4) ? 1 : (EV::kInterp ? COOT_INTERP4_MINB : 2);
 }
 
 template <class T, int ACC, class EV>

@@ -323,8 +323,8 @@ void fill_program(const coot_expr* e, coot::FusedArgs* a) {
   int sp = 0;
   for (uint32_t i = 0; i < e->n_instr; ++i) {
     const int op = e->prog[i].op, arg = e->prog[i].arg;
-    a->key[i] = (uint16_t)COOT_KEY(op, sp);  // dense dispatch index (coot_fused.cuh)
-    a->arg[i] = (uint8_t)arg;
+    // dense dispatch index (coot_fused.cuh) | argument << 16
+    a->code[i] = (uint32_t)COOT_KEY(op, sp) | ((uint32_t)arg << 16);
     if (op == COOT_OP_LOAD || op == COOT_OP_SCALAR) ++sp;
     else if (is_binary(op)) --sp;
   }

@@ -1,3 +1,5 @@
-OUT=gpurun_out/d2; mkdir -p $OUT
-timeout 900 python -m pytest tests -m gpu -q -x -k "dim or fp8 or half or narrow" > $OUT/pytest.txt 2>&1; tail -2 $OUT/pytest.txt
-python tools/sweep.py > $OUT/sweep.txt 2>&1
+OUT=gpurun_out/k2c; mkdir -p $OUT
+W=c2_interp,axpy_interp_2p30,poly_interp_2p30,f64_c2_interp_2p29,bf16_interp_c2
+L=$(ls $PWD/paper_2508_11385_b200/libcoot_*.so | head -1); N=$(basename $L .so)
+COOT_LIB_PATH=$L COOT_TMA_CTAS=3 python tools/sweep.py --only $W > $OUT/${N}_c3.txt 2>&1
+COOT_LIB_PATH=$L python tools/sweep.py --only $W > $OUT/${N}_c2.txt 2>&1
