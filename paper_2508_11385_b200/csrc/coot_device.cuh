@@ -932,6 +932,8 @@ struct Accum {
   T mn, mx;
   u64 n, idx;
   double c, s1, s2;
+  float cf;  // VAR on f32 / 16-bit / 8-bit: the shift c as f32 (exact: c is an element)
+  bool has;  // IMIN / IMAX: an element has been seen (hot-loop copy of idx != ~0)
   __device__ __forceinline__ void init() {
     s = S(0);
     mn = MinMaxId<T>::lo();
@@ -939,6 +941,8 @@ struct Accum {
     n = 0;
     idx = ~0ull;
     c = s1 = s2 = 0.0;
+    cf = 0.f;
+    has = false;
   }
   // Accumulate W consecutive elements whose first element has global index
   // `base` (only the index-returning kinds use it).
@@ -957,10 +961,11 @@ struct Accum {
         bw = better ? w : bw;
       }
       const bool better = (ACC == ACC_IMIN) ? lt(bv, mn) : lt(mx, bv);
-      if (idx == ~0ull || better) {
+      if (!has || better) {
         if constexpr (ACC == ACC_IMIN) mn = bv;
         else mx = bv;
         idx = base + (u64)bw;
+        has = true;
       }
     } else {
       add<W>(v);
@@ -969,7 +974,10 @@ struct Accum {
   template <int W>
   __device__ __forceinline__ void add(const T (&v)[W]) {
     if constexpr (ACC == ACC_VAR) {
-      if (n == 0) c = as_double(v[0]);  // the shift: the thread's first element
+      if (n == 0) {  // the shift: the thread's first element
+        c = as_double(v[0]);
+        if constexpr (!std::is_same<T, double>::value && is_float<T>()) cf = as_float(v[0]);
+      }
       if constexpr (std::is_same<T, double>::value || !is_float<T>()) {
         double a1 = 0.0, a2 = 0.0;  // the unit's shifted sums, then one update each
 #pragma unroll
@@ -984,7 +992,6 @@ struct Accum {
         // f32 / 16-bit: the unit's shifted sums in f32 (the shift is an element,
         // so exact in f32; x - c is exact when x is near c), widened to f64 once
         // per unit — relative error ~W * 2^-24, far inside the 1e-5 bar
-        const float cf = (float)c;
         float a1 = 0.f, a2 = 0.f, x[W];
         widen_f32<T, W>(v, x);
 #pragma unroll
@@ -1125,12 +1132,18 @@ struct Accum {
   }
 };
 
-// First statement of every kernel launched with programmatic stream
-// serialization (coot_launch.cuh launch_k): wait until the previous grid on
-// the stream has completed and its writes are visible, then let the next
-// kernel's CTAs be scheduled as soon as this grid's have all started.
-__device__ __forceinline__ void pdl_enter() {
+// Programmatic dependent launch (coot_launch.cuh launch_k).  pdl_wait() is the
+// first statement of every kernel launched that way: it blocks until the
+// previous grid on the stream has completed and its writes are visible.
+// pdl_trigger() — issued by the fused kernels once their streaming loop is
+// done — lets the next kernel's CTAs be scheduled during this one's final
+// reduction (without it they launch when this grid completes).  Triggering
+// at kernel start instead measured 10-20 % slower on low-register kernels
+// (var / index_min / norm2): the early CTAs sat on the SMs for the whole run.
+__device__ __forceinline__ void pdl_wait() {
   asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_trigger() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 

@@ -65,7 +65,7 @@ __device__ __forceinline__ void dim_eval(const In& in, const FusedArgs& f, T (&v
 // ---- K4a: block per (column, segment) — tall columns ------------------------
 template <class T, class EV>
 __global__ void __launch_bounds__(kThreads) dim0_block_kernel(const __grid_constant__ DimArgs d) {
-  pdl_enter();
+  pdl_wait();
   constexpr int W = Unit<T>::W;
   constexpr int K = EV::K;
   typedef typename SumT<T>::type S;
@@ -146,7 +146,7 @@ __global__ void __launch_bounds__(kThreads) dim0_block_kernel(const __grid_const
 // ---- K4b: warp per column — short columns (m < 2048) ------------------------
 template <class T, class EV>
 __global__ void __launch_bounds__(kThreads) dim0_warp_kernel(const __grid_constant__ DimArgs d) {
-  pdl_enter();
+  pdl_wait();
   constexpr int K = EV::K;
   const int lane = threadIdx.x & 31;
   const u64 warp = ((u64)blockIdx.x * kThreads + threadIdx.x) >> 5;
@@ -182,7 +182,7 @@ __device__ __forceinline__ void load_elem_strided(const FusedArgs& a, u64 i, u64
 
 template <class T, class EV>
 __global__ void __launch_bounds__(kThreads) dim_strided_kernel(const __grid_constant__ DimArgs d) {
-  pdl_enter();
+  pdl_wait();
   if (d.dim == 0) {
     const int lane = threadIdx.x & 31;
     const u64 warp = ((u64)blockIdx.x * kThreads + threadIdx.x) >> 5;
@@ -224,7 +224,7 @@ __global__ void __launch_bounds__(kThreads) dim_strided_kernel(const __grid_cons
 // block of the row tile.
 template <class T, class EV>
 __global__ void __launch_bounds__(kThreads) dim1_kernel(const __grid_constant__ DimArgs d) {
-  pdl_enter();
+  pdl_wait();
   constexpr int W = Unit<T>::W;
   constexpr int K = EV::K;
   typedef typename SumT<T>::type S;

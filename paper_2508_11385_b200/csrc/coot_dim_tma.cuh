@@ -47,7 +47,7 @@ __device__ __forceinline__ S consumer_reduce_sum(S v, S* ws) {
 // ---- dim 0 -------------------------------------------------------------------
 template <class T, class EV>
 __global__ void __launch_bounds__(kTmaThreads, tma_min_ctas<EV>()) dim0_tma_kernel(const __grid_constant__ DimArgs d) {
-  pdl_enter();
+  pdl_wait();
   constexpr int W = Unit<T>::W;
   constexpr int K = EV::K;
   typedef typename SumT<T>::type S;
@@ -175,7 +175,7 @@ __global__ void __launch_bounds__(kTmaThreads, tma_min_ctas<EV>()) dim0_tma_kern
 // ---- dim 1 -------------------------------------------------------------------
 template <class T, class EV>
 __global__ void __launch_bounds__(kTmaThreads, tma_min_ctas<EV>()) dim1_tma_kernel(const __grid_constant__ DimArgs d) {
-  pdl_enter();
+  pdl_wait();
   constexpr int W = Unit<T>::W;
   typedef typename SumT<T>::type S;
   constexpr u64 R = (u64)kConsumerWarps * 32 * W;  // rows per tile

@@ -281,7 +281,7 @@ __device__ __forceinline__ void load_elem(const FusedArgs& a, u64 e, T (&in)[EV:
 template <class T, int ACC, class EV, int U>
 __global__ void __launch_bounds__(kThreads, EV::kInterp ? 1 : COOT_CAT_MINB)
     fused_kernel(const __grid_constant__ FusedArgs a) {
-  pdl_enter();
+  pdl_wait();
   constexpr int W = Unit<T>::W;
   constexpr int K = EV::K;
   Accum<T, ACC> acc;
@@ -346,6 +346,7 @@ __global__ void __launch_bounds__(kThreads, EV::kInterp ? 1 : COOT_CAT_MINB)
     acc.template add_at<1>(v, e);
   }
 
+  pdl_trigger();  // streaming done: the next kernel may start launching
   if constexpr (ACC != ACC_NONE) {
     Accum<T, ACC> bt = block_reduce<T, ACC>(acc);
     grid_finish<T, ACC>(bt, a.partials, a.ticket, a.final_mode, a.kind, a.result, a.count, a.ex);
@@ -361,7 +362,7 @@ __global__ void __launch_bounds__(kThreads, EV::kInterp ? 1 : COOT_CAT_MINB)
 // catalog matching.
 template <class T, int ACC, class EV>
 __global__ void __launch_bounds__(kThreads) fused_strided_kernel(const __grid_constant__ FusedArgs a) {
-  pdl_enter();
+  pdl_wait();
   constexpr int K = EV::K;
   Accum<T, ACC> acc;
   acc.init();
@@ -390,6 +391,7 @@ __global__ void __launch_bounds__(kThreads) fused_strided_kernel(const __grid_co
       ++j;
     }
   }
+  pdl_trigger();  // streaming done: the next kernel may start launching
   if constexpr (ACC != ACC_NONE) {
     Accum<T, ACC> bt = block_reduce<T, ACC>(acc);
     grid_finish<T, ACC>(bt, a.partials, a.ticket, a.final_mode, a.kind, a.result, a.count, a.ex);
@@ -448,7 +450,7 @@ constexpr int tma_min_ctas() {
 template <class T, int ACC, class EV>
 __global__ void __launch_bounds__(kTmaThreads, tma_min_ctas<EV>())
     fused_tma_kernel(const __grid_constant__ FusedArgs a) {
-  pdl_enter();
+  pdl_wait();
   constexpr int W = Unit<T>::W;
   constexpr int K = EV::K;
   extern __shared__ __align__(128) unsigned char smem[];
@@ -551,6 +553,7 @@ __global__ void __launch_bounds__(kTmaThreads, tma_min_ctas<EV>())
     }
   }
 
+  pdl_trigger();  // streaming done: the next kernel may start launching
   if constexpr (ACC != ACC_NONE) {
     Accum<T, ACC> bt = block_reduce<T, ACC>(acc);
     grid_finish<T, ACC>(bt, a.partials, a.ticket, a.final_mode, a.kind, a.result, a.count, a.ex);
@@ -570,7 +573,7 @@ __global__ void __launch_bounds__(kTmaThreads, tma_min_ctas<EV>())
 template <class T, int ACC, class EV>
 __global__ void __launch_bounds__(kTmaThreads, tma_min_ctas<EV>())
     fused_cols_tma_kernel(const __grid_constant__ FusedArgs a) {
-  pdl_enter();
+  pdl_wait();
   constexpr int W = Unit<T>::W;
   constexpr int K = EV::K;
   extern __shared__ __align__(128) unsigned char smem[];
@@ -682,6 +685,7 @@ __global__ void __launch_bounds__(kTmaThreads, tma_min_ctas<EV>())
       for (u64 i = head + nun * W + threadIdx.x; i < len; i += kConsumerWarps * 32) scalar_elem(i);
     }
   }
+  pdl_trigger();  // streaming done: the next kernel may start launching
   if constexpr (ACC != ACC_NONE) {
     Accum<T, ACC> bt = block_reduce<T, ACC>(acc);
     grid_finish<T, ACC>(bt, a.partials, a.ticket, a.final_mode, a.kind, a.result, a.count, a.ex);

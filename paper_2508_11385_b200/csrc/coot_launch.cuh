@@ -99,11 +99,10 @@ inline cudaError_t allow_smem(const void* fn, unsigned bytes) {
 }
 
 // Programmatic dependent launch: the kernel may be scheduled while the previous
-// kernel on the stream is still running (once all of that grid's CTAs have
-// executed griddepcontrol.launch_dependents); every kernel launched this way
-// begins with pdl_enter(), whose griddepcontrol.wait blocks until the previous
-// grid has completed and its memory is visible — so only the launch latency
-// overlaps, never the data.
+// kernel on the stream is still finishing (once every CTA of that grid has
+// executed pdl_trigger() or exited); every kernel launched this way begins
+// with pdl_wait(), which blocks until the previous grid has completed and its
+// memory is visible — so only the launch latency overlaps, never the data.
 template <class Args>
 cudaError_t launch_k(void (*k)(const Args), unsigned grid, unsigned block, unsigned smem,
                      cudaStream_t s, const Args& a, int pdl) {

@@ -35,6 +35,7 @@ struct coot_ctx {
   int tma_smem_kb = 0;      // TMA driver: stage-ring budget override in KB (0 = policy)
   int dim_tma = 0;          // sum(X,dim): TMA-staged kernels when the layout allows
   int pdl = 1;              // programmatic dependent launch of fused / dim kernels
+  int smem_per_sm = 0, smem_reserved = 0;  // bytes (device attributes)
   coot::Rec* recs = nullptr;  // per-block records of the fused pass
   unsigned max_grid = 0;
   unsigned* ticket = nullptr;  // fused-pass arrival counter
@@ -46,6 +47,22 @@ struct coot_ctx {
   bool log = false;
   const coot::Exchange* pending_ex = nullptr;  // set by coot_reduce_exchange for one call
 };
+
+// Dynamic shared memory of a persistent TMA-driver CTA, padded so that at most
+// `per_sm` CTAs fit on one SM.  The grid is sized for per_sm CTAs per SM; a
+// low-footprint kernel (few registers, a 64 KB ring) would otherwise fit a
+// third CTA, and under programmatic dependent launch — where a kernel's CTAs
+// are placed while the previous kernel still holds some SMs — the scheduler
+// then stacks 3 CTAs on the SMs that freed first and 1 on the others:
+// measured 10-20 % slower (var / index_min / norm2 at 2^30).
+static unsigned pad_smem(const coot_ctx* ctx, unsigned smem, u64 per_sm) {
+  if (ctx->smem_per_sm <= 0) return smem;
+  const u64 floor = (u64)ctx->smem_per_sm / (per_sm + 1) + 1024 -
+                    std::min<u64>((u64)ctx->smem_reserved, (u64)ctx->smem_per_sm / (per_sm + 1));
+  const u64 cap = (u64)ctx->smem_per_sm / per_sm - (u64)ctx->smem_reserved;
+  return (unsigned)std::max<u64>(smem, std::min<u64>(floor, std::min<u64>(cap, 200u << 10)));
+}
+
 
 namespace {
 
@@ -511,7 +528,7 @@ coot_status run_strided(coot_ctx* ctx, const coot_expr* e, const Shape& sh, int 
     a.tile_units = (uint32_t)tu;
     a.stages = (uint32_t)stages;
     p.driver = 3;
-    p.smem = (unsigned)(stages * stage_bytes + 16 * stages);
+    p.smem = pad_smem(ctx, (unsigned)(stages * stage_bytes + 16 * stages), ctx->tma_ctas_per_sm);
     p.grid = (unsigned)std::max<u64>(1, std::min<u64>(e->n_cols * S, G));
   }
   if (ctx->log)
@@ -592,6 +609,7 @@ coot_status run_fused(coot_ctx* ctx, const coot_expr* e, const Shape& sh, int ac
     // a ring too big for two CTAs per SM (> ~113 KB) runs one persistent CTA per SM
     const u64 per_sm = p.smem > (110u << 10) ? 1 : (u64)ctx->tma_ctas_per_sm;
     grid = std::max<u64>(1, std::min<u64>(grid, (u64)ctx->sm_count * per_sm));
+    p.smem = pad_smem(ctx, p.smem, per_sm);
   } else {
     const u64 work = std::max<u64>(a.nunits, scalar_work);
     grid = std::max<u64>(1, ceil_div(work, coot::kThreads));
@@ -686,7 +704,7 @@ coot_status run_dim(coot_ctx* ctx, const coot_expr* e, const Shape& sh, uint32_t
     const u64 stages = std::max<u64>(2, std::min<u64>(8, (96u << 10) / stage_bytes));
     d.f.tile_units = coot::kTileUnits;
     d.f.stages = (uint32_t)stages;
-    p.smem = (unsigned)(stages * stage_bytes + 16 * stages);
+    p.smem = pad_smem(ctx, (unsigned)(stages * stage_bytes + 16 * stages), ctx->tma_ctas_per_sm);
     p.grid = (unsigned)std::min<u64>(n * S, G);
     if (S > 1) {
       part_bytes = n * S * sbytes;
@@ -710,7 +728,7 @@ coot_status run_dim(coot_ctx* ctx, const coot_expr* e, const Shape& sh, uint32_t
     const u64 stage_bytes = nk * cg * R1 * es;
     const u64 stages = std::max<u64>(2, std::min<u64>(8, (96u << 10) / stage_bytes));
     d.f.stages = (uint32_t)stages;
-    p.smem = (unsigned)(stages * stage_bytes + 16 * stages);
+    p.smem = pad_smem(ctx, (unsigned)(stages * stage_bytes + 16 * stages), ctx->tma_ctas_per_sm);
     p.grid = (unsigned)std::min<u64>(nrt * nchunks, G);
     if (nchunks > 1) {
       part_bytes = nchunks * m * sbytes;
@@ -932,6 +950,8 @@ coot_status coot_init(coot_ctx** out, int device, void* cuda_stream, uint32_t fl
   // back-to-back calls overlap each launch with the previous kernel's tail
   // (COOT_PDL=0: plain stream-ordered launches)
   ctx->pdl = env_int("COOT_PDL", 1) ? 1 : 0;
+  cudaDeviceGetAttribute(&ctx->smem_per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, device);
+  cudaDeviceGetAttribute(&ctx->smem_reserved, cudaDevAttrReservedSharedMemoryPerBlock, device);
   ctx->max_grid = (unsigned)ctx->sm_count * 32u;
   e = cudaMalloc(&ctx->recs, sizeof(coot::Rec) * ctx->max_grid);
   if (e == cudaSuccess) e = cudaMalloc(&ctx->ticket, 64 * sizeof(unsigned));

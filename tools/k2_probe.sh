@@ -1,5 +1,6 @@
-OUT=gpurun_out/k2c; mkdir -p $OUT
-W=c2_interp,axpy_interp_2p30,poly_interp_2p30,f64_c2_interp_2p29,bf16_interp_c2
-L=$(ls $PWD/paper_2508_11385_b200/libcoot_*.so | head -1); N=$(basename $L .so)
-COOT_LIB_PATH=$L COOT_TMA_CTAS=3 python tools/sweep.py --only $W > $OUT/${N}_c3.txt 2>&1
-COOT_LIB_PATH=$L python tools/sweep.py --only $W > $OUT/${N}_c2.txt 2>&1
+OUT=gpurun_out/pdl3; mkdir -p $OUT
+W=var_2p30,imin_2p30,mean_2p30,norm2_2p30,accu_2p30,c2_eval_accu,c2_reduce,dot_2p30,c3_dim1,c4_u32,axpy_accu_2p30
+COOT_PDL=0 python tools/sweep.py --only $W > $OUT/nopdl.txt 2>&1
+COOT_PDL=1 python tools/sweep.py --only $W > $OUT/pdl.txt 2>&1
+python tools/latency_parts.py > $OUT/parts.txt 2>&1
+timeout 900 python -m pytest tests -m gpu -q -x > $OUT/pytest.txt 2>&1; tail -2 $OUT/pytest.txt

@@ -22,6 +22,8 @@ WL = {
     "c2ro_e4m3": ("e4m3", 1 << 15, 1 << 16, "L0 L1 MUL EXP S0 L2 MUL ADD", [3.0], "ACCU", False),
     "c3d1_e4m3": ("e4m3", 65536, 32768, "L0", [], "SUM_DIM1", False),
     "c3d1_bf16": ("bf16", 32768, 32768, "L0", [], "SUM_DIM1", False),
+    "var": ("f32", 1 << 30, 1, "L0", [], "VAR", False),
+    "imin": ("f32", 1 << 30, 1, "L0", [], "INDEX_MIN", False),
     "axpy": ("f32", 1 << 30, 1, "S0 L0 MUL L1 ADD", [2.5], "ACCU", True),
     "c3d0": ("f64", 32768, 32768, "L0", [], "SUM_DIM0", False),
     "c3d1": ("f64", 32768, 32768, "L0", [], "SUM_DIM1", False),
@@ -42,7 +44,8 @@ for s, t in enumerate(ops):
     ctx.fill(t, "randu", stream=s, n_rows=m)
 out = torch.empty(m * n, dtype=api.TORCH_DTYPE[elem], device="cuda") if store else None
 rlen = n if kind == "SUM_DIM0" else (m if kind == "SUM_DIM1" else 2)
-res = torch.empty(rlen, dtype=api.RESULT_DTYPE[elem], device="cuda")
+res = torch.empty(rlen, dtype=torch.int64 if kind.startswith("INDEX") else api.RESULT_DTYPE[elem],
+                  device="cuda")
 torch.cuda.synchronize()
 for _ in range(reps):
     ctx.reduce(elem, m, n, prog, ops, sc, kind, res, out)
