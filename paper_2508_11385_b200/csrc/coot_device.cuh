@@ -125,6 +125,7 @@ struct FusedArgs {
   uint32_t n_instr;
   uint32_t tile_units;  // TMA driver: 16-byte units per tile (multiple of 256)
   uint32_t stages;      // TMA driver: smem pipeline depth
+  uint32_t producer_sleep;  // TMA drivers: the producer sleeps while the ring is full
   // strided (view) path: element (i, j) of operand k at in[k][i*inc[k] + j*ld[k]]
   u64 m;                // rows of the expression
   u64 ld[COOT_MAX_OPERANDS], inc[COOT_MAX_OPERANDS];
@@ -742,18 +743,39 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 // Block until the phase with the given parity has completed.
+// Wait for an mbarrier phase.  SLEEP: the thread is suspended until the phase
+// completes or a 100 us hint runs out (else the short system limit applies and
+// the thread re-polls).  Used for the producer's wait for a free stage when the
+// program is compute-heavy (FusedArgs::producer_sleep): there a re-polling
+// producer warp takes issue slots from the consumers (bf16 / f16 / E4M3 c2
+// +2-3 %); memory-bound programs keep polling (prompt re-issue of the ring).
+template <bool SLEEP = false>
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t addr = smem_u32(bar);
   uint32_t done;
   do {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(done)
-        : "r"(addr), "r"(parity)
-        : "memory");
+    if constexpr (SLEEP) {
+      asm volatile(
+          "{\n\t.reg .pred p;\n\t"
+          "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+          "selp.u32 %0, 1, 0, p;\n\t}"
+          : "=r"(done)
+          : "r"(addr), "r"(parity), "n"(100000)
+          : "memory");
+    } else {
+      asm volatile(
+          "{\n\t.reg .pred p;\n\t"
+          "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+          "selp.u32 %0, 1, 0, p;\n\t}"
+          : "=r"(done)
+          : "r"(addr), "r"(parity)
+          : "memory");
+    }
   } while (!done);
+}
+__device__ __forceinline__ void producer_wait(uint64_t* bar, uint32_t parity, uint32_t sleep) {
+  if (sleep) mbar_wait<true>(bar, parity);
+  else mbar_wait<false>(bar, parity);
 }
 // L2 policy for data that is streamed exactly once.
 __device__ __forceinline__ uint64_t policy_evict_first() {

@@ -481,7 +481,7 @@ __global__ void __launch_bounds__(kTmaThreads, tma_min_ctas<EV>())
       uint32_t s = 0, ph = 0;
       u64 i = 0;
       for (u64 t = blockIdx.x; t < ntiles; t += gridDim.x, ++i) {
-        if (i >= S) mbar_wait(&empty[s], ph ^ 1u);
+        if (i >= S) producer_wait(&empty[s], ph ^ 1u, a.producer_sleep);
         const u64 u0 = t * TU;
         const uint32_t nu = (uint32_t)((a.nunits - u0) < TU ? (a.nunits - u0) : TU);
         mbar_expect_tx(&full[s], nu * 16u * nk);
@@ -614,7 +614,7 @@ __global__ void __launch_bounds__(kTmaThreads, tma_min_ctas<EV>())
         u64 j, r0, len, head, nun;
         piece(p, j, r0, len, head, nun);
         for (u64 u0 = 0; u0 < nun; u0 += TU, ++i) {
-          if (i >= S) mbar_wait(&empty[s], ph ^ 1u);
+          if (i >= S) producer_wait(&empty[s], ph ^ 1u, a.producer_sleep);
           const uint32_t nu = (uint32_t)((nun - u0) < TU ? (nun - u0) : TU);
           mbar_expect_tx(&full[s], nu * 16u * nk);
           for (uint32_t k = 0; k < nk; ++k)

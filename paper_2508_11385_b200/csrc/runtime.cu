@@ -35,6 +35,7 @@ struct coot_ctx {
   int tma_smem_kb = 0;      // TMA driver: stage-ring budget override in KB (0 = policy)
   int dim_tma = 0;          // sum(X,dim): TMA-staged kernels when the layout allows
   int pdl = 1;              // programmatic dependent launch of fused / dim kernels
+  int producer_sleep = -1;  // TMA producer sleeps on a full ring: -1 policy, 0 never, 1 always
   int smem_per_sm = 0, smem_reserved = 0;  // bytes (device attributes)
   coot::Rec* recs = nullptr;  // per-block records of the fused pass
   unsigned max_grid = 0;
@@ -47,6 +48,20 @@ struct coot_ctx {
   bool log = false;
   const coot::Exchange* pending_ex = nullptr;  // set by coot_reduce_exchange for one call
 };
+
+// Whether the TMA producer should sleep (rather than poll) while the ring is
+// full: for compute-heavy programs — EXP / LOG / SQRT / DIV, or run on the
+// interpreter — where the consumers, not HBM, set the pace (coot_device.cuh
+// mbar_wait).
+static uint32_t producer_sleep(const coot_ctx* ctx, const coot_expr* e, int catalog) {
+  if (ctx->producer_sleep >= 0) return (uint32_t)ctx->producer_sleep;
+  if (catalog < 0) return 1;
+  for (uint32_t i = 0; i < e->n_instr; ++i) {
+    const unsigned op = e->prog[i].op;
+    if (op == COOT_OP_EXP || op == COOT_OP_LOG || op == COOT_OP_SQRT || op == COOT_OP_DIV) return 1;
+  }
+  return 0;
+}
 
 // Dynamic shared memory of a persistent TMA-driver CTA, padded so that at most
 // `per_sm` CTAs fit on one SM.  The grid is sized for per_sm CTAs per SM; a
@@ -527,6 +542,7 @@ coot_status run_strided(coot_ctx* ctx, const coot_expr* e, const Shape& sh, int 
     a.nseg = (uint32_t)S;
     a.tile_units = (uint32_t)tu;
     a.stages = (uint32_t)stages;
+    a.producer_sleep = producer_sleep(ctx, e, -1);
     p.driver = 3;
     p.smem = pad_smem(ctx, (unsigned)(stages * stage_bytes + 16 * stages), ctx->tma_ctas_per_sm);
     p.grid = (unsigned)std::max<u64>(1, std::min<u64>(e->n_cols * S, G));
@@ -603,6 +619,7 @@ coot_status run_fused(coot_ctx* ctx, const coot_expr* e, const Shape& sh, int ac
     const u64 stages = std::max<u64>(2, std::min<u64>(8, ring / tile_bytes_all));
     a.tile_units = (uint32_t)tu;
     a.stages = (uint32_t)stages;
+    a.producer_sleep = producer_sleep(ctx, e, p.catalog);
     p.smem = (unsigned)(stages * tile_bytes_all + 2 * stages * 8);
     const u64 ntiles = ceil_div(a.nunits, tu);
     grid = std::max<u64>(ntiles, ceil_div(scalar_work, coot::kConsumerWarps * 32));
@@ -950,6 +967,7 @@ coot_status coot_init(coot_ctx** out, int device, void* cuda_stream, uint32_t fl
   // back-to-back calls overlap each launch with the previous kernel's tail
   // (COOT_PDL=0: plain stream-ordered launches)
   ctx->pdl = env_int("COOT_PDL", 1) ? 1 : 0;
+  ctx->producer_sleep = std::max(-1, std::min(1, env_int("COOT_PRODUCER_SLEEP", -1)));
   cudaDeviceGetAttribute(&ctx->smem_per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, device);
   cudaDeviceGetAttribute(&ctx->smem_reserved, cudaDevAttrReservedSharedMemoryPerBlock, device);
   ctx->max_grid = (unsigned)ctx->sm_count * 32u;
