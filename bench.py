@@ -251,6 +251,8 @@ def measure_other_configs(coot, ctx, peak, reps=10):
 def cpu_baseline_oracle():
     """The oracle timed on this host on the full c2 workload (1e8 elements),
     single-threaded; input generation untimed.  Returns (record, accu)."""
+    import numpy as np
+
     import oracle
     n = M_ROWS * N_COLS
     ops = [oracle.fill("f32", "randu", n, stream=s) for s in range(3)]
@@ -258,12 +260,39 @@ def cpu_baseline_oracle():
     z = oracle.eval_program("f32", PROGRAM, ops, SCALARS)
     r = oracle.reduce("f32", "ACCU", z)
     dt = time.perf_counter() - t0
-    del ops, z
+    del z
     gbs = n * BYTES_PER_ELEM / dt / 1e9
     rec = {"value": gbs, "unit": "GB/s", "cores": 1, "kind": "oracle",
            "sample": f"full c2 workload on rank 0's block ({n} elements), one pass, "
                      f"{dt:.2f} s single-threaded, generation untimed",
            "elements_per_s": n / dt}
+    # SURVEY §8(d) variant (ii): the same oracle on T host threads over
+    # contiguous chunks (the C calls release the GIL), chunk sums combined in
+    # chunk order in f64 — context only; parity uses the 1-thread result
+    try:
+        import concurrent.futures as cf
+        T = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+        T = max(1, min(T or 1, 64))
+        bounds = [(n * k // T, n * (k + 1) // T) for k in range(T)]
+
+        def chunk(b):
+            lo, hi = b
+            zz = oracle.eval_program("f32", PROGRAM, [o[lo:hi] for o in ops], SCALARS)
+            return float(oracle.reduce("f64", "ACCU", zz.astype(np.float64)))
+
+        with cf.ThreadPoolExecutor(max_workers=T) as ex:
+            t0 = time.perf_counter()
+            parts = list(ex.map(chunk, bounds))
+            dtm = time.perf_counter() - t0
+        tot = 0.0
+        for p_ in parts:
+            tot += p_
+        rec["threads"] = {"value": n * BYTES_PER_ELEM / dtm / 1e9, "unit": "GB/s", "cores": T,
+                          "seconds": dtm, "speedup_vs_1_thread": dt / dtm,
+                          "accu_rel_diff_vs_1_thread": abs(tot - float(r)) / abs(float(r))}
+    except Exception as exc:  # informational only
+        rec["threads"] = {"error": str(exc)[:200]}
+    del ops
     return rec, float(r)
 
 
