@@ -28,7 +28,8 @@ struct coot_ctx {
   uint32_t flags = 0;
   int sm_count = 0;
   int cc_major = 0, cc_minor = 0;
-  int blocks_per_sm = 8;    // LDG driver / dim kernels: CTAs per SM in the grid
+  int blocks_per_sm = 8;    // LDG fused driver / strided views: CTAs per SM in the grid
+  int dim_blocks_per_sm = 4;  // LDG dim-sum kernels: CTAs per SM the work is split over
   int driver = 1;           // fused pass: 1 = TMA-staged (default), 0 = LDG
   int tma_ctas_per_sm = 2;  // TMA driver: CTAs per SM in the grid
   int tma_tile_units = 0;   // TMA driver: units per operand tile override (0 = policy)
@@ -684,7 +685,7 @@ coot_status run_dim(coot_ctx* ctx, const coot_expr* e, const Shape& sh, uint32_t
   for (uint32_t k = 0; k < e->n_operands; ++k)
     same = same && ((reinterpret_cast<uintptr_t>(e->operands[k].ptr) & 15) == mis);
   const bool col_aligned = ((m * es) % 16) == 0;
-  const u64 target = (u64)ctx->sm_count * ctx->blocks_per_sm;
+  const u64 target = (u64)ctx->sm_count * ctx->dim_blocks_per_sm;
   coot::DimPlan p;
   p.pdl = ctx->pdl;
   p.catalog = ((ctx->flags & COOT_INIT_FORCE_INTERP) == 0 && e->n_instr == 1) ? 0 : -1;
@@ -954,6 +955,9 @@ coot_status coot_init(coot_ctx** out, int device, void* cuda_stream, uint32_t fl
                 device, maj, min);
   }
   ctx->blocks_per_sm = std::max(1, std::min(32, env_int("COOT_BLOCKS_PER_SM", 8)));
+  // dim sums: 4 per SM measured best (bf16 / E4M3 sum(X,1) +7 / +18 % over 8,
+  // f64 c3 +2 %; tools/k2_probe.sh sweep)
+  ctx->dim_blocks_per_sm = std::max(1, std::min(32, env_int("COOT_DIM_BLOCKS_PER_SM", 4)));
   ctx->driver = env_int("COOT_DRIVER", 1) ? 1 : 0;
   ctx->tma_ctas_per_sm = std::max(1, std::min(4, env_int("COOT_TMA_CTAS", 2)));
   // TMA ring geometry overrides (tuning; 0 = the default policy of run_fused):
