@@ -913,15 +913,63 @@ __device__ __forceinline__ float pairwise_f32(const float (&x)[W]) {
   }
 }
 
+// ---- 16-bit views of narrow elements and the mixed-precision add ------------
+// Every bf16 / f16 / E4M3 / E5M2 value is exactly a 16-bit value: bf16 itself,
+// the others f16 (8-bit types decoded two per cvt).  add.rn.f32.{f16,bf16}
+// (sm_100 FHADD) adds such a value to an f32 and rounds once — exactly
+// RN(widen(a) + c), one instruction instead of a widening plus an FADD.
+template <class T>
+__device__ __forceinline__ void to_h16(const T (&v)[2], unsigned short (&h)[2]) {
+  if constexpr (is_half<T>()) {
+    h[0] = v[0].bits;
+    h[1] = v[1].bits;
+  } else {
+    const unsigned short pk = (unsigned short)(v[0].bits | ((unsigned)v[1].bits << 8));
+    unsigned h2;
+    if constexpr (std::is_same<T, e4m3>::value)
+      asm("cvt.rn.f16x2.e4m3x2 %0, %1;" : "=r"(h2) : "h"(pk));
+    else
+      h2 = __byte_perm((unsigned)pk, 0u, 0x1404);
+    h[0] = (unsigned short)(h2 & 0xffffu);
+    h[1] = (unsigned short)(h2 >> 16);
+  }
+}
+template <class T>
+__device__ __forceinline__ float h16_to_f32(unsigned short h) {
+  if constexpr (std::is_same<T, bf16>::value) return __uint_as_float((unsigned)h << 16);
+  else return __half2float(__ushort_as_half(h));
+}
+template <class T>
+__device__ __forceinline__ float add_f32_h16(float c, unsigned short h) {
+  float d;
+  if constexpr (std::is_same<T, bf16>::value)
+    asm("add.rn.f32.bf16 %0, %1, %2;" : "=f"(d) : "h"(h), "f"(c));
+  else
+    asm("add.rn.f32.f16 %0, %1, %2;" : "=f"(d) : "h"(h), "f"(c));
+  return d;
+}
+// widen(a) + widen(b), rounded once to f32, from the 16-bit views
+template <class T>
+__device__ __forceinline__ float pair_sum_h16(unsigned short a, unsigned short b) {
+  return add_f32_h16<T>(h16_to_f32<T>(a), b);
+}
+
 template <class T, int W>
 __device__ __forceinline__ typename SumT<T>::type unit_sum(const T (&v)[W]) {
-  if constexpr (is_narrow<T>()) {
-    // widen exactly, pairwise sum in f32 (error ~2^-24, far below the format's
-    // 2^-9 / 2^-12 rounding; E4M3 unit sums are exact), one conversion to f64
-    // per unit
-    float x[W];
-    widen_f32<T, W>(v, x);
-    return (double)pairwise_f32<W>(x);
+  if constexpr (is_narrow<T>() && W >= 2) {
+    // pairwise sum in f32 of the exact values (error ~2^-24, far below the
+    // format's 2^-9 / 2^-12 rounding; E4M3 unit sums are exact), the first
+    // level as mixed-precision adds; one conversion to f64 per unit
+    float x[W / 2];
+#pragma unroll
+    for (int w = 0; w < W / 2; ++w) {
+      unsigned short h[2];
+      to_h16<T>({v[2 * w], v[2 * w + 1]}, h);
+      x[w] = pair_sum_h16<T>(h[0], h[1]);
+    }
+    return (double)pairwise_f32<W / 2>(x);
+  } else if constexpr (is_narrow<T>()) {
+    return (double)as_float(v[0]);
   } else if constexpr (is_float<T>()) {
     if constexpr (W == 1) {
       return (double)v[0];
