@@ -649,10 +649,43 @@ __device__ __forceinline__ void half_round_vec(const float (&y)[W], H (&v)[W]) {
   if constexpr (W & 1) v[W - 1] = half_from_f32<H>(y[W - 1]);
 }
 
+// + - * on 16-bit pairs with the packed instructions ({add,sub,mul}.rn.{bf16x2,
+// f16x2}: one HADD2/HMUL2/HFMA2 per pair instead of widen x4, two f32 ops and a
+// narrowing).  Same bits as the f32 route: each returns the exact result
+// rounded once (RNE, subnormals kept — no .ftz), and the f32 route's double
+// rounding is innocuous (R24: 24 >= 2p + 2), so both equal RNE16(exact).
+// `.rn` is explicit, so ptxas may not contract a MUL into a following ADD.
+template <int OP, class H>
+__device__ __forceinline__ uint32_t half2_op(uint32_t x, uint32_t y) {
+  uint32_t d;
+  if constexpr (std::is_same<H, bf16>::value) {
+    if constexpr (OP == COOT_OP_ADD) asm("add.rn.bf16x2 %0, %1, %2;" : "=r"(d) : "r"(x), "r"(y));
+    else if constexpr (OP == COOT_OP_SUB) asm("sub.rn.bf16x2 %0, %1, %2;" : "=r"(d) : "r"(x), "r"(y));
+    else asm("mul.rn.bf16x2 %0, %1, %2;" : "=r"(d) : "r"(x), "r"(y));
+  } else {
+    if constexpr (OP == COOT_OP_ADD) asm("add.rn.f16x2 %0, %1, %2;" : "=r"(d) : "r"(x), "r"(y));
+    else if constexpr (OP == COOT_OP_SUB) asm("sub.rn.f16x2 %0, %1, %2;" : "=r"(d) : "r"(x), "r"(y));
+    else asm("mul.rn.f16x2 %0, %1, %2;" : "=r"(d) : "r"(x), "r"(y));
+  }
+  return d;
+}
+template <int OP, class H, int W>
+__device__ __forceinline__ void half2_vec(H (&a)[W], const H (&b)[W]) {
+#pragma unroll
+  for (int w = 0; w + 1 < W; w += 2) {
+    const uint32_t d = half2_op<OP, H>((uint32_t)a[w].bits | ((uint32_t)a[w + 1].bits << 16),
+                                       (uint32_t)b[w].bits | ((uint32_t)b[w + 1].bits << 16));
+    a[w] = H((unsigned short)(d & 0xffffu), true);
+    a[w + 1] = H((unsigned short)(d >> 16), true);
+  }
+  if constexpr (W & 1) a[W - 1] = half_bin<OP, H>(a[W - 1], b[W - 1]);
+}
+
 template <int OP, class T, int W>
 __device__ __forceinline__ void bin_vec(T (&a)[W], const T (&b)[W]) {
-  if constexpr (is_half<T>() && (OP == COOT_OP_ADD || OP == COOT_OP_SUB || OP == COOT_OP_MUL ||
-                                 OP == COOT_OP_DIV)) {
+  if constexpr (is_half<T>() && (OP == COOT_OP_ADD || OP == COOT_OP_SUB || OP == COOT_OP_MUL)) {
+    half2_vec<OP, T, W>(a, b);
+  } else if constexpr (is_half<T>() && OP == COOT_OP_DIV) {
     float y[W];
 #pragma unroll
     for (int w = 0; w < W; ++w) y[w] = bin<OP>(to_f32(a[w]), to_f32(b[w]));
@@ -665,7 +698,9 @@ __device__ __forceinline__ void bin_vec(T (&a)[W], const T (&b)[W]) {
 
 template <int OP, class T, int W>
 __device__ __forceinline__ void un_vec(T (&v)[W]) {
-  if constexpr (is_half<T>() && (OP == COOT_OP_SQUARE || OP == COOT_OP_SQRT)) {
+  if constexpr (is_half<T>() && OP == COOT_OP_SQUARE) {
+    half2_vec<COOT_OP_MUL, T, W>(v, v);
+  } else if constexpr (is_half<T>() && OP == COOT_OP_SQRT) {
     float y[W];
 #pragma unroll
     for (int w = 0; w < W; ++w) y[w] = un<OP>(to_f32(v[w]));

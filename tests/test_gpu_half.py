@@ -97,13 +97,16 @@ def test_unary_exhaustive(ctxs, etype, op):
 
 
 @pytest.mark.parametrize("etype", HALF)
-@pytest.mark.parametrize("op", ["ADD", "MUL", "DIV"])
+@pytest.mark.parametrize("op", ["ADD", "SUB", "MUL", "DIV"])
 def test_binary_dense_sample(ctxs, etype, op):
     """One operand exhaustive (all finite patterns), the other a fixed spread of
-    magnitudes: subnormal, overflow and tie cases of the single rounding."""
+    magnitudes: subnormal, overflow and tie cases of the single rounding.  The
+    subnormal b (2^-130 bf16, 2^-20 f16) makes ADD / SUB of two subnormals
+    exact-or-tie cases that a flush-to-zero packed instruction would get wrong."""
     pats = np.arange(1 << 16, dtype=np.uint16)
     a = pats if etype == "bf16" else pats.view(np.float16)
-    for bval in (3.0, -0.375, 1.0 / 3.0, 1e-3, 300.0):
+    sub = 2.0 ** -130 if etype == "bf16" else 2.0 ** -20
+    for bval in (3.0, -0.375, 1.0 / 3.0, 1e-3, 300.0, sub, -3 * sub):
         b = np.full(a.size, oracle.half_from_double(etype, bval), dtype=np.uint16)
         b = b if etype == "bf16" else b.view(np.float16)
         prog = P(f"L0 L1 {op}")
