@@ -1,6 +1,6 @@
 """Run a few launches of one workload's fused kernel (for ncu captures).
 
-usage: python tools/profile_step.py [c1|c2|c2ro|axpy|c3d0|c3d1|c4u|c4s|dot|norm2] [reps]
+usage: python tools/profile_step.py [c1|c2|c2ro|c2i|axpy|c3d0|c3d1|c4u|c4s|dot|norm2] [reps]
 """
 import os
 import sys
@@ -17,6 +17,8 @@ P = lambda s: [(t, 0) if not (t[0] in "LS" and t[1:].isdigit()) else  # noqa: E7
 WL = {
     "c2": ("f32", 10000, 10000, "L0 L1 MUL EXP S0 L2 MUL ADD", [3.0], "ACCU", True),
     "c2ro": ("f32", 10000, 10000, "L0 L1 MUL EXP S0 L2 MUL ADD", [3.0], "ACCU", False),
+    # interpreter (K2) on the c2 program: the ctx is created with COOT_INIT_FORCE_INTERP
+    "c2i": ("f32", 10000, 10000, "L0 L1 MUL EXP S0 L2 MUL ADD", [3.0], "ACCU", True),
     "c1": ("f32", 1_000_000, 1, "S0 L0 MUL L1 ADD", [2.5], "ACCU", True),
     "c2ro_bf16": ("bf16", 1 << 15, 1 << 15, "L0 L1 MUL EXP S0 L2 MUL ADD", [3.0], "ACCU", False),
     "c2ro_e4m3": ("e4m3", 1 << 15, 1 << 16, "L0 L1 MUL EXP S0 L2 MUL ADD", [3.0], "ACCU", False),
@@ -37,7 +39,7 @@ name = sys.argv[1] if len(sys.argv) > 1 else "c2"
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
 elem, m, n, prog, sc, kind, store = WL[name]
 prog = P(prog)
-ctx = coot.Context(0)
+ctx = coot.Context(0, flags=2 if name in ("c2i",) else 0)  # 2 = COOT_INIT_FORCE_INTERP
 k = 1 + max(a for o, a in prog if o == "LOAD")
 ops = [torch.empty(m * n, dtype=api.TORCH_DTYPE[elem], device="cuda") for _ in range(k)]
 for s, t in enumerate(ops):
