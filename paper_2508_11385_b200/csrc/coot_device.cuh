@@ -1022,6 +1022,27 @@ __device__ __forceinline__ typename SumT<T>::type unit_sum(const T (&v)[W]) {
   }
 }
 
+// Sums of squares inside a unit in f32 (norm2, var): trusted when the f32 sum
+// u is a normal number >= 2^-100 — then no square overflowed (u would be inf)
+// and squares that fell below 2^-126 are < 2^-26 of u.  Anything else (inf,
+// NaN, tiny, 0) sends the unit to f64.  Only bf16 and f32 values can leave the
+// range (f16 / E4M3 / E5M2 squares are exact normal f32 values or 0).
+template <class T>
+__host__ __device__ constexpr bool sq_range_checked() {
+  return std::is_same<T, float>::value || std::is_same<T, bf16>::value;
+}
+__device__ __forceinline__ bool sq_sum_ok(float u) {
+  return u >= 0x1p-100f && u <= 3.40282347e38f;
+}
+// sum of exact f64 squares of W f32 values, in element order
+template <int W>
+__device__ __forceinline__ double sumsq_f64(const float (&x)[W]) {
+  double r = 0.0;
+#pragma unroll
+  for (int w = 0; w < W; ++w) r = __fma_rn((double)x[w], (double)x[w], r);
+  return r;
+}
+
 // Per-thread / per-block / per-rank accumulator for every reduction kind.
 //  ACC_SUM, ACC_SUMSQ: s (f64 for floats, u64 modular for ints)
 //  ACC_MINMAX:         mn, mx
@@ -1105,19 +1126,43 @@ struct Accum {
           a1 = __fadd_rn(a1, d);
           a2 = __fmaf_rn(d, d, a2);
         }
-        s1 = __dadd_rn(s1, (double)a1);
-        s2 = __dadd_rn(s2, (double)a2);
+        if (__builtin_expect(!sq_range_checked<T>() || sq_sum_ok(a2), 1)) {
+          s1 = __dadd_rn(s1, (double)a1);
+          s2 = __dadd_rn(s2, (double)a2);
+        } else {
+          // squared deviations left f32's range (x - c or a square overflowed,
+          // or all are tiny), or the unit equals the shift: shifted sums in f64
+          double b1 = 0.0, b2 = 0.0;
+#pragma unroll
+          for (int w = 0; w < W; ++w) {
+            const double e = __dsub_rn((double)x[w], c);
+            b1 = __dadd_rn(b1, e);
+            b2 = __fma_rn(e, e, b2);
+          }
+          s1 = __dadd_rn(s1, b1);
+          s2 = __dadd_rn(s2, b2);
+        }
       }
       n += W;
     } else if constexpr (ACC == ACC_SUM) {
       s = sum_add<S>(s, unit_sum<T, W>(v));
     } else if constexpr (ACC == ACC_SUMSQ) {
-      if constexpr (is_narrow<T>()) {  // squares of 16/8-bit values are exact in f32
+      if constexpr (is_narrow<T>() || std::is_same<T, float>::value) {
+        // squares in f32 (exact for 16/8-bit values), summed pairwise in f32.
+        // bf16 / f32 only: a unit whose f32 sum is not a normal number >= 2^-100
+        // (a square overflowed, or every square is tiny and may have lost its
+        // bits, or the unit is zero / non-finite) is redone in f64 — so norm2
+        // is accurate over the whole range at one compare per unit
         float q[W];
         widen_f32<T, W>(v, q);
+        float qq[W];
 #pragma unroll
-        for (int w = 0; w < W; ++w) q[w] = __fmul_rn(q[w], q[w]);
-        s = sum_add<S>(s, (double)pairwise_f32<W>(q));
+        for (int w = 0; w < W; ++w) qq[w] = __fmul_rn(q[w], q[w]);
+        const float u = pairwise_f32<W>(qq);
+        if (__builtin_expect(!sq_range_checked<T>() || sq_sum_ok(u), 1))
+          s = sum_add<S>(s, (double)u);
+        else
+          s = sum_add<S>(s, sumsq_f64<W>(q));
       } else {
         T q[W];
 #pragma unroll
