@@ -106,6 +106,21 @@ def test_integer_accu_modular():
     assert int(oracle.reduce("s64", "ACCU", s)) == want
 
 
+@pytest.mark.parametrize("etype", ["f32", "f64"])
+def test_norm2_scale_invariance_far_from_one(etype):
+    """norm2(2^e * v) = 2^e * norm2(v) exactly (power-of-two scaling is exact and
+    commutes with the correctly rounded result) for e far outside where v^2 is a
+    normal number of eT: pins the oracle's squares as wider than eT."""
+    dt = oracle.DTYPES[etype]
+    v = np.array([3, 4, 12, 84], dt)                     # norm2 = 85
+    big, small = ((2.0 ** 100, 2.0 ** -100) if etype == "f32" else (2.0 ** 600, 2.0 ** -600))
+    assert oracle.reduce(etype, "NORM2", v) == 85
+    assert oracle.reduce(etype, "NORM2", (v * dt(big)).astype(dt)) == dt(85 * big)
+    assert oracle.reduce(etype, "NORM2", (v * dt(small)).astype(dt)) == dt(85 * small)
+    for k in range(0, 6):
+        assert oracle.reduce(etype, "NORM2", np.full(4**k, small, dt)) == dt(2**k * small)
+
+
 def test_norm2_rejected_for_integers():
     with pytest.raises(oracle.OracleError):
         oracle.reduce("u32", "NORM2", np.ones(3, np.uint32))
