@@ -159,6 +159,14 @@ struct CatalogEval<StaticProg<Code...>> {
 // source (a shared-memory address under the TMA driver).  One dispatch
 // evaluates UD whole 16-byte units.
 #define COOT_KEY(op, d) ((op) * 9 + (d))
+// Fused-operand dispatch ops (host peephole, runtime.cu fill_program): an ADD,
+// SUB or MUL whose right operand is an operand load or a scalar, "L k OP" -> OP_L k and
+// "S k OP" -> OP_S k (and "S k L j OP" -> "L j" OP_S k for the commutative ADD /
+// MUL), so the loaded / broadcast value never takes a stack slot or a dispatch
+// of its own.  Same arithmetic, same operand order (a OP b, b = the fused
+// operand) as the unfused sequence.  c2: 8 dispatches -> 6, axpy 5 -> 3.
+#define COOT_XOP_L(op) (14 + (op) - COOT_OP_ADD)  // ADD, SUB, MUL -> 14..16
+#define COOT_XOP_S(op) (17 + (op) - COOT_OP_ADD)  // ADD, SUB, MUL -> 17..19
 
 template <int KMAX, int SMAX>
 struct InterpEval {
@@ -198,6 +206,27 @@ struct InterpEval {
       __trap(); /* op illegal for T: rejected on the host (R9) */          \
     }                                                                      \
     break;
+#define COOT_BINL_CASE(OP, d)                                              \
+  case COOT_KEY(COOT_XOP_L(COOT_OP_##OP), d):                              \
+    if constexpr ((d) >= 1 && (d) <= SMAX && op_legal<T>(COOT_OP_##OP)) {  \
+      CT t[W];                                                             \
+      load_to<T, W>(src, (int)arg, t);                                     \
+      bin_vec<COOT_OP_##OP>(st[(d) >= 1 ? (d) - 1 : 0], t);                \
+    } else if constexpr ((d) >= 1 && (d) <= SMAX) {                        \
+      __trap();                                                            \
+    }                                                                      \
+    break;
+#define COOT_BINS_CASE(OP, d)                                              \
+  case COOT_KEY(COOT_XOP_S(COOT_OP_##OP), d):                              \
+    if constexpr ((d) >= 1 && (d) <= SMAX && op_legal<T>(COOT_OP_##OP)) {  \
+      const CT s = scalar_as<CT>(a.scalars[arg]);                          \
+      CT t[W];                                                             \
+      _Pragma("unroll") for (int w = 0; w < W; ++w) t[w] = s;              \
+      bin_vec<COOT_OP_##OP>(st[(d) >= 1 ? (d) - 1 : 0], t);                \
+    } else if constexpr ((d) >= 1 && (d) <= SMAX) {                        \
+      __trap();                                                            \
+    }                                                                      \
+    break;
 #define COOT_D(M, ...) M(__VA_ARGS__ 0) M(__VA_ARGS__ 1) M(__VA_ARGS__ 2) M(__VA_ARGS__ 3) \
   M(__VA_ARGS__ 4) M(__VA_ARGS__ 5) M(__VA_ARGS__ 6) M(__VA_ARGS__ 7) M(__VA_ARGS__ 8)
 
@@ -223,11 +252,19 @@ struct InterpEval {
         COOT_D(COOT_BIN_CASE, DIV,)
         COOT_D(COOT_BIN_CASE, MIN,)
         COOT_D(COOT_BIN_CASE, MAX,)
+        COOT_D(COOT_BINL_CASE, ADD,)
+        COOT_D(COOT_BINL_CASE, SUB,)
+        COOT_D(COOT_BINL_CASE, MUL,)
+        COOT_D(COOT_BINS_CASE, ADD,)
+        COOT_D(COOT_BINS_CASE, SUB,)
+        COOT_D(COOT_BINS_CASE, MUL,)
         default:
           break;
       }
     }
 #undef COOT_D
+#undef COOT_BINS_CASE
+#undef COOT_BINL_CASE
 #undef COOT_BIN_CASE
 #undef COOT_UN_CASE
 #undef COOT_SCALAR_CASE

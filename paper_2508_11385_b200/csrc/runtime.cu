@@ -353,14 +353,41 @@ void fill_program(const coot_expr* e, coot::FusedArgs* a) {
     a->ld[k] = k < e->n_operands ? op_ld(e->operands[k]) : 0;
     a->inc[k] = k < e->n_operands ? op_inc(e->operands[k]) : 0;
   }
+  // dense dispatch index (coot_fused.cuh) | argument << 16, with the fused-
+  // operand peephole (COOT_XOP_L / COOT_XOP_S): a push directly followed by an
+  // ADD / SUB / MUL that consumes it becomes one dispatch (the device has fused
+  // cases for those three only: more cases cost the small interpreter spills).  The stack is never
+  // deeper than in the original program.
   int sp = 0;
-  for (uint32_t i = 0; i < e->n_instr; ++i) {
+  uint32_t n = 0;
+  const uint32_t ni = e->n_instr;
+  auto emit = [&](int key, int arg) { a->code[n++] = (uint32_t)key | ((uint32_t)arg << 16); };
+  // COOT_NO_FUSED_OPERANDS=1: plain one-dispatch-per-instruction code (A/B aid)
+  static const bool force_plain = env_int("COOT_NO_FUSED_OPERANDS", 0) != 0;
+  for (uint32_t i = 0; i < ni; ++i) {
     const int op = e->prog[i].op, arg = e->prog[i].arg;
-    // dense dispatch index (coot_fused.cuh) | argument << 16
-    a->code[i] = (uint32_t)COOT_KEY(op, sp) | ((uint32_t)arg << 16);
+    const int nx = i + 1 < ni ? e->prog[i + 1].op : -1;
+    const int nx2 = i + 2 < ni ? e->prog[i + 2].op : -1;
+    if (!force_plain && sp >= 1 && (op == COOT_OP_LOAD || op == COOT_OP_SCALAR) &&
+        (nx == COOT_OP_ADD || nx == COOT_OP_SUB || nx == COOT_OP_MUL)) {
+      emit(COOT_KEY(op == COOT_OP_LOAD ? COOT_XOP_L(nx) : COOT_XOP_S(nx), sp), arg);
+      ++i;  // the push and its op: depth unchanged
+      continue;
+    }
+    if (!force_plain && op == COOT_OP_SCALAR && nx == COOT_OP_LOAD &&
+        (nx2 == COOT_OP_ADD || nx2 == COOT_OP_MUL)) {
+      // s OP x == x OP s bit for bit for + and * (IEEE, packed 16-bit, modular)
+      emit(COOT_KEY(COOT_OP_LOAD, sp), e->prog[i + 1].arg);
+      emit(COOT_KEY(COOT_XOP_S(nx2), sp + 1), arg);
+      i += 2;
+      ++sp;
+      continue;
+    }
+    emit(COOT_KEY(op, sp), arg);
     if (op == COOT_OP_LOAD || op == COOT_OP_SCALAR) ++sp;
     else if (is_binary(op)) --sp;
   }
+  a->n_instr = n;
 }
 
 int acc_for_kind(uint32_t kind) {
