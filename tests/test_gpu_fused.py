@@ -362,3 +362,41 @@ def test_ldg_driver_parity(ctx_ldg, etype):
         if etype == "f64" and has_transcendental(prog):
             continue
         assert_elementwise(got, want, etype, max_ulp=2 if has_transcendental(prog) else 0)
+
+
+# Fused-operand dispatch (runtime.cu fill_program): every ADD / SUB / MUL whose
+# right operand is a LOAD or SCALAR push, at every depth the small (<= 4) and
+# large (<= 8) interpreter classes reach, the commutative "S k L j OP" swap, and
+# non-commutative forms that must NOT be swapped (s - x, s / x, min/max).
+FUSED_FORMS = [
+    "L0 L1 ADD", "L0 L1 SUB", "L0 L1 MUL", "L0 S0 ADD", "L0 S0 SUB", "L0 S1 MUL",
+    "S0 L0 ADD", "S0 L0 MUL", "S0 L0 SUB", "S1 L1 MAX", "S0 L1 MIN",
+    "L0 L1 L2 SUB SUB", "L0 L1 L2 L3 SUB S0 MUL SUB L2 MUL SUB",
+    "L0 S0 L1 MUL SUB", "L2 S1 L0 ADD L1 SUB MUL", "L0 L1 L2 S0 L3 MUL ADD ADD SUB",
+    "L0 L1 L2 L3 L4 L5 L6 S0 SUB L7 MUL ADD SUB MUL ADD SUB MUL",
+    "L0 L1 L2 L3 L4 L5 L6 S1 ADD L7 SUB MUL SUB ADD MUL SUB ADD",
+    "S0 L0 L1 L2 SUB MUL SUB S1 L3 MUL ADD",
+]
+
+
+@pytest.mark.parametrize("etype", ["f32", "f64", "u32", "s64", "bf16"])
+def test_interpreter_fused_operand_forms(ctx_interp, etype):
+    n = 4099
+    sc = {"f32": [2.5, -0.75], "f64": [2.5, -0.75], "u32": [7, 3], "s64": [7, -3],
+          "bf16": [2.5, -0.75]}[etype]
+    for form in FUSED_FORMS:
+        prog = P(form)
+        k = n_operands(prog)
+        if etype == "bf16":
+            ops = [oracle.fill(etype, "randu", n, stream=s) for s in range(k)]
+        else:
+            ops = make_inputs(etype, n, k, seed=len(form))
+        want = oracle.eval_program(etype, prog, ops, sc)
+        got = run_eval(ctx_interp, etype, prog, ops, sc)
+        if etype == "bf16":
+            w, g = np.asarray(want).view(np.uint16), np.asarray(got).view(np.uint16)
+            nan_w = np.isnan(oracle.to_float(etype, want))
+            assert np.array_equal(nan_w, np.isnan(oracle.to_float(etype, got))), form
+            assert np.array_equal(g[~nan_w], w[~nan_w]), form
+        else:
+            assert_elementwise(got, want, etype, max_ulp=0), form
