@@ -32,6 +32,7 @@ struct coot_ctx {
   int dim_blocks_per_sm = 4;  // LDG dim-sum kernels: CTAs per SM the work is split over
   int driver = 1;           // fused pass: 1 = TMA-staged (default), 0 = LDG
   int tma_ctas_per_sm = 2;  // TMA driver: CTAs per SM in the grid
+  bool tma_ctas_env = false;  // COOT_TMA_CTAS given (tuning runs): keep it as is
   int tma_tile_units = 0;   // TMA driver: units per operand tile override (0 = policy)
   int tma_smem_kb = 0;      // TMA driver: stage-ring budget override in KB (0 = policy)
   int dim_tma = 0;          // sum(X,dim): TMA-staged kernels when the layout allows
@@ -652,7 +653,11 @@ coot_status run_fused(coot_ctx* ctx, const coot_expr* e, const Shape& sh, int ac
     const u64 ntiles = ceil_div(a.nunits, tu);
     grid = std::max<u64>(ntiles, ceil_div(scalar_work, coot::kConsumerWarps * 32));
     // a ring too big for two CTAs per SM (> ~113 KB) runs one persistent CTA per SM
-    const u64 per_sm = p.smem > (110u << 10) ? 1 : (u64)ctx->tma_ctas_per_sm;
+    u64 per_sm = p.smem > (110u << 10) ? 1 : (u64)ctx->tma_ctas_per_sm;
+    // fewer tiles than per_sm CTAs on every SM (small n, e.g. c1's 1e6): one CTA
+    // per SM, so no SM streams for two CTAs while others host one, and the
+    // finish merges fewer records (tools/small_n.py: n = 1e6 4.8 -> 4.4 us)
+    if (grid < (u64)ctx->sm_count * per_sm && !ctx->tma_ctas_env) per_sm = 1;
     grid = std::max<u64>(1, std::min<u64>(grid, (u64)ctx->sm_count * per_sm));
     p.smem = pad_smem(ctx, p.smem, per_sm);
   } else {
@@ -987,6 +992,7 @@ coot_status coot_init(coot_ctx** out, int device, void* cuda_stream, uint32_t fl
   ctx->dim_blocks_per_sm = std::max(1, std::min(32, env_int("COOT_DIM_BLOCKS_PER_SM", 4)));
   ctx->driver = env_int("COOT_DRIVER", 1) ? 1 : 0;
   ctx->tma_ctas_per_sm = std::max(1, std::min(4, env_int("COOT_TMA_CTAS", 2)));
+  ctx->tma_ctas_env = env_int("COOT_TMA_CTAS", 0) != 0;  // explicit: no small-n policy
   // TMA ring geometry overrides (tuning; 0 = the default policy of run_fused):
   // tile = a multiple of 512 units, ring budget in KB per CTA
   const int tile_env = env_int("COOT_TMA_TILE", 0), kb_env = env_int("COOT_TMA_SMEM_KB", 0);
