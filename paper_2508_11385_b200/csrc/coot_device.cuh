@@ -1470,6 +1470,30 @@ __device__ __forceinline__ void grid_finish(const Accum<T, ACC>& block_total, Re
                                             uint32_t kind, void* result, u64 count,
                                             const Exchange& ex) {
   __shared__ bool am_last;
+  if (gridDim.x == 1) {
+    // a one-CTA grid (n of one tile or less): the same arithmetic as the last-
+    // block path below — its one record merged into an empty accumulator, then
+    // a block tree — without the record store, the ticket atomic and the
+    // record load (three dependent L2 round trips)
+    Accum<T, ACC> acc;
+    acc.init();
+    if (threadIdx.x == 0) {
+      Accum<T, ACC> o;
+      o.from_rec(block_total.to_rec(0));
+      acc.merge(o);
+    }
+    const Accum<T, ACC> tot = block_reduce<T, ACC>(acc);
+    if (threadIdx.x == 0) {
+      if (final_mode == FINAL_PARTIAL) {
+        *reinterpret_cast<Rec*>(result) = tot.to_rec(count);
+      } else if (final_mode == FINAL_EXCHANGE) {
+        exchange_finish<T, ACC>(tot.to_rec(count), ex, kind, result);
+      } else {
+        write_final<T, ACC>(tot, kind, result, count);
+      }
+    }
+    return;
+  }
   if (threadIdx.x == 0) {
     partials[blockIdx.x] = block_total.to_rec(0);
     // acq_rel: releases this block's record, and (for the last arrival)
