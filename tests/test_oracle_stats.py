@@ -34,6 +34,24 @@ def test_closed_forms(etype):
 
 
 @pytest.mark.parametrize("etype", ["f32", "f64"])
+def test_var_scale_invariance_far_from_one(etype):
+    """var(2^e v) = 2^(2e) var(v) exactly for power-of-two scalings that put the
+    deviations' squares outside eT's range (the device's f64 route, R12/R22):
+    pins the oracle's squares and sums as wider than eT."""
+    dt = oracle.DTYPES[etype]
+    v = np.array([1.0, 4.0, 1.0, 4.0, 7.0], dt)          # mean 3.4, var 6.3
+    base = oracle.stats(etype, "VAR", v)
+    e = 62 if etype == "f32" else 500
+    for k in (e, -e):
+        s = 2.0 ** k
+        got = oracle.stats(etype, "VAR", (v * dt(s)).astype(dt))
+        want = to_np(round_fraction(exact_var(v) * Fraction(2) ** (2 * k), etype), etype)
+        assert got == want, (k, got, want)
+        if np.isfinite(want) and want != 0 and np.isfinite(base * dt(s) * dt(s)):
+            assert got == base * dt(s) * dt(s)
+
+
+@pytest.mark.parametrize("etype", ["f32", "f64"])
 def test_random_against_exact_rationals(etype):
     rng = np.random.default_rng(12)
     dt = oracle.DTYPES[etype]
