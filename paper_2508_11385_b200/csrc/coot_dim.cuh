@@ -223,7 +223,7 @@ __global__ void __launch_bounds__(kThreads) dim_strided_kernel(const __grid_cons
 // combined in g order through shared memory; chunks in cc order by the last
 // block of the row tile.
 template <class T, class EV>
-__global__ void __launch_bounds__(kThreads) dim1_kernel(const __grid_constant__ DimArgs d) {
+__device__ __forceinline__ void dim1_body(const DimArgs& d) {
   pdl_wait();
   constexpr int W = Unit<T>::W;
   constexpr int K = EV::K;
@@ -365,6 +365,20 @@ __global__ void __launch_bounds__(kThreads) dim1_kernel(const __grid_constant__ 
     }
   }
   if (threadIdx.x == 0) d.tickets[rt] = 0u;
+}
+
+template <class T, class EV>
+__global__ void __launch_bounds__(kThreads) dim1_kernel(const __grid_constant__ DimArgs d) {
+  dim1_body<T, EV>(d);
+}
+// 8-bit types: <= 85 registers so 3 CTAs fit per SM (86 registers allowed only
+// 2, and the host's 4-per-SM grid ran in two waves: E4M3 sum(X,1) at 50 % of
+// DRAM bandwidth, long-scoreboard bound with 16 warps per SM)
+// (a separate kernel: an explicit minBlocks = 1 on the others changed their
+// register allocation and cost bf16 sum(X,1) 17 %)
+template <class T, class EV>
+__global__ void __launch_bounds__(kThreads, 3) dim1_kernel_b8(const __grid_constant__ DimArgs d) {
+  dim1_body<T, EV>(d);
 }
 
 }  // namespace coot

@@ -153,7 +153,7 @@ struct Dim0Warp {
 };
 template <class T, class EV>
 struct Dim1 {
-  static constexpr DimFn run = &dim1_kernel<T, EV>;
+  static constexpr DimFn run = sizeof(T) == 1 ? &dim1_kernel_b8<T, EV> : &dim1_kernel<T, EV>;
 };
 template <class T, class EV>
 struct DimStrided {

@@ -816,7 +816,10 @@ coot_status run_dim(coot_ctx* ctx, const coot_expr* e, const Shape& sh, uint32_t
     const u64 nrt = ceil_div(m, R);
     // one CTA per (row tile, chunk): keep the grid within one resident wave
     // (floor, not ceil) so no small tail wave is left over
-    u64 nchunks = std::max<u64>(1, target / nrt);
+    // 8-bit elements: dim1_kernel is built for 3 resident CTAs per SM (its 32 KB
+    // of f64 row partials and __launch_bounds__(256, 3)), so one wave is 3 per SM
+    const u64 tgt1 = es == 1 ? std::min<u64>(target, (u64)ctx->sm_count * 3) : target;
+    u64 nchunks = std::max<u64>(1, tgt1 / nrt);
     nchunks = std::min<u64>(nchunks, std::max<u64>(1, n / (8 * Gc)));
     const u64 ccols = ceil_div(n, nchunks);
     nchunks = ceil_div(n, ccols);
