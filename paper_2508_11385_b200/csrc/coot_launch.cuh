@@ -151,10 +151,23 @@ template <class T, class EV>
 struct Dim0Warp {
   static constexpr DimFn run = &dim0_warp_kernel<T, EV>;
 };
-template <class T, class EV>
-struct Dim1 {
-  static constexpr DimFn run = sizeof(T) == 1 ? &dim1_kernel_b8<T, EV> : &dim1_kernel<T, EV>;
+// dim1_kernel_b8 only for catalog programs: capped at 85 registers the
+// interpreter spills 400-700 B per thread (252-255 registers uncapped)
+template <class EV>
+struct IsInterp : std::false_type {};
+template <int S, int I>
+struct IsInterp<InterpEval<S, I>> : std::true_type {};
+// (a specialisation, not ?: — taking both addresses instantiated both kernels)
+template <class T, class EV, bool B8>
+struct Dim1Pick {
+  static constexpr DimFn run = &dim1_kernel<T, EV>;
 };
+template <class T, class EV>
+struct Dim1Pick<T, EV, true> {
+  static constexpr DimFn run = &dim1_kernel_b8<T, EV>;
+};
+template <class T, class EV>
+struct Dim1 : Dim1Pick<T, EV, sizeof(T) == 1 && !IsInterp<EV>::value> {};
 template <class T, class EV>
 struct DimStrided {
   static constexpr DimFn run = &dim_strided_kernel<T, EV>;
