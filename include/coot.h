@@ -180,6 +180,9 @@ typedef struct coot_ctx coot_ctx;
  * backend selection (CUDA only).  *out receives the ctx. */
 coot_status coot_init(coot_ctx** out, int device, void* cuda_stream, uint32_t flags);
 coot_status coot_destroy(coot_ctx* ctx);
+/* Re-bind the ctx to another stream.  Work enqueued later on the new stream
+ * is ordered after everything already enqueued through the ctx on the old
+ * one (an event wait on the device; the host does not block). */
 coot_status coot_set_stream(coot_ctx* ctx, void* cuda_stream);
 
 /* Host-only checks (no CUDA call): ABI version, element type, limits, operand
@@ -251,8 +254,13 @@ coot_status coot_shard_range(uint64_t n, uint32_t rank, uint32_t nranks, uint64_
  *   before with these mailboxes (e.g. a call counter starting at 1).  Every
  *   rank must make the matching call; a rank that never arrives makes the
  *   others time out (~20 s) with a device fault (COOT_ERR_DEVICE on the next
- *   synchronising call).  MIN/MAX/MINMAX/INDEX of a globally empty
- *   expression return the identities / ~0. */
+ *   synchronising call).  Each published record carries its epoch; a rank
+ *   that finds a peer's flag past `epoch` but no record of `epoch` (the peer
+ *   skipped a call) also faults instead of combining stale data.  Advance the
+ *   epoch only after a call returned COOT_OK (a call rejected on the host
+ *   enqueues nothing and must be retried with the same epoch).
+ *   MIN/MAX/MINMAX/INDEX of a globally empty expression return the
+ *   identities / ~0. */
 #define COOT_MAX_RANKS 8
 #define COOT_IPC_HANDLE_BYTES 64
 coot_status coot_mailbox_create(coot_ctx* ctx, void** mailbox, void* ipc_handle);

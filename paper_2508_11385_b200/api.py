@@ -169,9 +169,17 @@ def init(device: int = 0, print_info: bool = False) -> Context:
 
 
 def default_ctx(device: int | None = None) -> Context:
+    """The default ctx for `device`, re-bound to torch's CURRENT stream on every
+    call: work issued inside ``with torch.cuda.stream(s)`` is enqueued on s, in
+    order with the torch ops that produced its operands.  (An explicitly passed
+    Context keeps the stream it was created with / set_stream'ed to.)"""
     if device is None:
         device = torch.cuda.current_device()
-    return init(device)
+    ctx = init(device)
+    cur = torch.cuda.current_stream(ctx.device)
+    if cur.cuda_stream != ctx.stream.cuda_stream:
+        ctx.set_stream(cur)
+    return ctx
 
 
 def partial_bytes(kind: str, length: int = 1) -> int:

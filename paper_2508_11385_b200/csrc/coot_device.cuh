@@ -1440,7 +1440,7 @@ __device__ void exchange_finish(const Rec& mine, const Exchange& ex, uint32_t ki
     __stcg(&slot->a, mine.a);
     __stcg(&slot->b, mine.b);
     __stcg(&slot->count, mine.count);
-    __stcg(&slot->pad, 0ull);
+    __stcg(&slot->pad, ex.epoch);  // which call this record belongs to
   }
   __threadfence_system();
   for (uint32_t p = 0; p < P; ++p)
@@ -1456,6 +1456,10 @@ __device__ void exchange_finish(const Rec& mine, const Exchange& ex, uint32_t ki
     }
   }
   const Rec* slots = reinterpret_cast<const Rec*>(ex.mbox[ex.rank]) + half;
+  // every record must be this call's: a peer whose flag passed `epoch` without
+  // writing epoch's record (it skipped a call) is a protocol fault, not data
+  for (uint32_t q = 0; q < P; ++q)
+    if (__ldcg(&slots[q].pad) != ex.epoch) __trap();
   combine_in_order<T, ACC>(P, [&](uint32_t q) { return load_rec_cg(slots + q); }, kind, result);
 }
 

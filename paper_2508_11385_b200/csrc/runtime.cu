@@ -49,6 +49,7 @@ struct coot_ctx {
   coot_stats_t stats{};
   bool log = false;
   const coot::Exchange* pending_ex = nullptr;  // set by coot_reduce_exchange for one call
+  cudaEvent_t handoff = nullptr;  // orders a new stream after the old one (coot_set_stream)
 };
 
 // Whether the TMA producer should sleep (rather than poll) while the ring is
@@ -1014,9 +1015,11 @@ coot_status coot_init(coot_ctx** out, int device, void* cuda_stream, uint32_t fl
   e = cudaMalloc(&ctx->recs, sizeof(coot::Rec) * ctx->max_grid);
   if (e == cudaSuccess) e = cudaMalloc(&ctx->ticket, 64 * sizeof(unsigned));
   if (e == cudaSuccess) e = cudaMemset(ctx->ticket, 0, 64 * sizeof(unsigned));
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ctx->handoff, cudaEventDisableTiming);
   if (e != cudaSuccess) {
     cudaFree(ctx->recs);
     cudaFree(ctx->ticket);
+    if (ctx->handoff) cudaEventDestroy(ctx->handoff);
     delete ctx;
     return fail(COOT_ERR_RESOURCE, "resource: cannot allocate reduction scratch (%s)", cudaGetErrorString(e));
   }
@@ -1041,6 +1044,7 @@ coot_status coot_destroy(coot_ctx* ctx) {
   cudaFree(ctx->ticket);
   cudaFree(ctx->dim_part);
   cudaFree(ctx->dim_tickets);
+  if (ctx->handoff) cudaEventDestroy(ctx->handoff);
   delete ctx;
   return ok();
 }
@@ -1048,11 +1052,17 @@ coot_status coot_destroy(coot_ctx* ctx) {
 coot_status coot_set_stream(coot_ctx* ctx, void* cuda_stream) {
   coot_status st = check_ctx(ctx);
   if (st != COOT_OK) return st;
-  if (reinterpret_cast<cudaStream_t>(cuda_stream) != ctx->stream) {
-    // the ticket counters are stream-ordered: drain the old stream first
-    cudaError_t e = cudaStreamSynchronize(ctx->stream);
-    if (e != cudaSuccess) return cuda_fail(e, "cudaStreamSynchronize");
-    ctx->stream = reinterpret_cast<cudaStream_t>(cuda_stream);
+  const cudaStream_t next = reinterpret_cast<cudaStream_t>(cuda_stream);
+  if (next != ctx->stream) {
+    // the scratch (records, tickets, dim partials) is used stream-ordered: the
+    // new stream waits (on the device, the host does not block) for everything
+    // already enqueued on the old one
+    st = bind_device(ctx);
+    if (st != COOT_OK) return st;
+    cudaError_t e = cudaEventRecord(ctx->handoff, ctx->stream);
+    if (e == cudaSuccess) e = cudaStreamWaitEvent(next, ctx->handoff, 0);
+    if (e != cudaSuccess) return cuda_fail(e, "stream hand-off");
+    ctx->stream = next;
   }
   return ok();
 }

@@ -150,12 +150,15 @@ class MailboxExchange:
         rank.  Every rank must call it the same number of times."""
         if not self.ok:
             raise RuntimeError("MailboxExchange: some rank could not map every peer's mailbox")
-        self.epoch += 1
         dtype = torch.int64 if kind.startswith("INDEX") else RESULT_DTYPE[lw.elem]
         res = torch.empty(2, dtype=dtype, device=self.ctx.device)
+        # the epoch advances only once the kernel is enqueued: a call rejected on
+        # the host (validation) leaves it unchanged, so a retry reuses it and a
+        # peer waiting at this epoch is never released by a later one
         self.ctx.reduce_exchange(lw.elem, lw.n_rows, lw.n_cols, lw.program, lw.operands,
-                                 lw.scalars, kind, self.mailboxes, self.rank, self.epoch, res,
-                                 out)
+                                 lw.scalars, kind, self.mailboxes, self.rank, self.epoch + 1,
+                                 res, out)
+        self.epoch += 1
         return res
 
     def close(self):

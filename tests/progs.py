@@ -137,7 +137,10 @@ def assert_reduction(got, want, etype, kind, abs_scale=None):
     tol = TOL[etype]
     for g, o in zip(got.astype(np.float64), want.astype(np.float64)):
         if o == 0:
-            scale = abs_scale if abs_scale is not None else 1.0
+            # the oracle's sum is exactly 0: only a cancellation residue relative
+            # to the magnitudes summed (abs_scale = sum |v_i|) is tolerated, and
+            # without that scale the result must be exactly 0
+            scale = abs_scale if abs_scale is not None else 0.0
             assert abs(g) <= tol * scale, (g, o)
         else:
             assert abs(g - o) <= tol * abs(o), (g, o, abs(g - o) / abs(o))

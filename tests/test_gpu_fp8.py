@@ -127,13 +127,21 @@ def test_reductions(ctxs, etype, kind, n):
                              abs_scale=float(np.abs(oracle.to_float(etype, z)).sum()) or 1.0)
 
 
+# (1000, 333): scalar paths (m % 16 != 0); (4096, 1000) and (2048, 4099): m a
+# multiple of the row tile with several column chunks, so dim1_kernel_b8's
+# vector path (widen + pairwise f32 over a 16-byte unit) and the chunk combine run
+DIM_SHAPES = [(1000, 333), (4096, 1000), (2048, 4099)]
+
+
 @pytest.mark.parametrize("etype", FP8)
 @pytest.mark.parametrize("dim", [0, 1])
-def test_sum_dims(ctxs, etype, dim):
-    m, n = 1000, 333
+@pytest.mark.parametrize("shape", DIM_SHAPES)
+@pytest.mark.parametrize("which", ["tma", "interp"])
+def test_sum_dims(ctxs, etype, dim, shape, which):
+    m, n = shape
     X = oracle.fill(etype, "randu", m * n, stream=8)
     want = oracle.sum_dim(etype, dim, X, m, n)
-    got, _ = run(ctxs["tma"], etype, P("L0"), [X], [], f"SUM_DIM{dim}", store=False,
+    got, _ = run(ctxs[which], etype, P("L0"), [X], [], f"SUM_DIM{dim}", store=False,
                  shape=(m, n))
     assert got.dtype == np.float32
     np.testing.assert_allclose(got, want, rtol=1e-6, atol=0)

@@ -156,15 +156,22 @@ def test_reductions(ctxs, etype, kind, n):
             assert half_ulp(got, np.atleast_1d(want)).max() <= 1, (name, got, want)
 
 
+# (1000, 333): the row tile (1024 rows) exceeds m, scalar path; (4096, 1000)
+# and (2048, 4099): whole row tiles and several column chunks (vector path)
+DIM_SHAPES = [(1000, 333), (4096, 1000), (2048, 4099)]
+
+
 @pytest.mark.parametrize("etype", HALF)
 @pytest.mark.parametrize("dim", [0, 1])
-def test_sum_dims(ctxs, etype, dim):
-    m, n = 1000, 333
+@pytest.mark.parametrize("shape", DIM_SHAPES)
+@pytest.mark.parametrize("which", ["tma", "interp"])
+def test_sum_dims(ctxs, etype, dim, shape, which):
+    m, n = shape
     X = oracle.fill(etype, "randu", m * n, stream=8)
     want = oracle.sum_dim(etype, dim, X, m, n)
     dev = to_dev(X, etype)
     r = torch.zeros(n if dim == 0 else m, dtype=TORCH[etype], device="cuda")
-    ctxs["tma"].reduce(etype, m, n, P("L0"), [dev], [], f"SUM_DIM{dim}", r)
+    ctxs[which].reduce(etype, m, n, P("L0"), [dev], [], f"SUM_DIM{dim}", r)
     torch.cuda.synchronize()
     assert half_ulp(to_host(r, etype), want).max() <= 1
 
