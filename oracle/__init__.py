@@ -76,6 +76,9 @@ def lib():
         L.orc_eval.restype = i32
         L.orc_eval.argtypes = [i32, u64, ctypes.POINTER(vp), i32, vp, i32,
                                ctypes.POINTER(i32), ctypes.POINTER(i32), i32, vp]
+        L.orc_eval_batch.restype = i32
+        L.orc_eval_batch.argtypes = [i32, u64, ctypes.POINTER(vp), i32, vp, i32, vp, vp, vp,
+                                     ctypes.c_int64, vp]
         L.orc_acc_size.restype = ctypes.c_size_t
         L.orc_acc_init.restype = i32
         L.orc_acc_init.argtypes = [vp, i32, i32]
@@ -163,6 +166,27 @@ def eval_program(etype: str, program, operands, scalars=()) -> np.ndarray:
     out = np.empty(n, dtype=dt)
     _check(lib().orc_eval(TYPES[etype], n, ptrs, len(ops_), _ptr(sc), len(scalars), opc, argc,
                           ni, _ptr(out)), "eval")
+    return out
+
+
+def eval_programs(etype: str, programs, operands, scalars=()) -> np.ndarray:
+    """eval_program for many programs over the same operands (one C call);
+    returns an array of shape (len(programs), n)."""
+    dt = DTYPES[etype]
+    ops_ = [np.ascontiguousarray(o, dtype=dt) for o in operands]
+    n = ops_[0].size
+    ptrs = (ctypes.c_void_p * max(len(ops_), 1))(*[o.ctypes.data for o in ops_])
+    sc = _scalar_array(etype, scalars)
+    lens = np.array([len(p) for p in programs], dtype=np.int64)
+    offs = np.zeros(len(programs) + 1, dtype=np.int64)
+    np.cumsum(lens, out=offs[1:])
+    flat = [x for p in programs for x in p]
+    opc = np.array([OPS[o] for o, _ in flat], dtype=np.int32)
+    argc = np.array([int(a) for _, a in flat], dtype=np.int32)
+    out = np.empty((len(programs), n), dtype=dt)
+    _check(lib().orc_eval_batch(TYPES[etype], n, ptrs, len(ops_), _ptr(sc), len(scalars),
+                                _ptr(opc), _ptr(argc), _ptr(offs), len(programs), _ptr(out)),
+           "eval_batch")
     return out
 
 

@@ -548,6 +548,24 @@ fail:
   return rc;
 }
 
+/* Many programs over the same operands: program p is ops/args[offs[p] ..
+ * offs[p+1]) and its element-wise result goes to out + p*n*es.  Plumbing for
+ * the brute-force program tests (one C call for 10^5 programs instead of one
+ * ctypes round trip each); each program is exactly one orc_eval. */
+int orc_eval_batch(int type, uint64_t n, const void* const* operands, int n_operands,
+                   const void* scalars, int n_scalars, const int* ops, const int* args,
+                   const int64_t* offs, int64_t n_progs, void* out) {
+  size_t es = esize(type);
+  if (es == 0) return ORC_E_TYPE;
+  for (int64_t p = 0; p < n_progs; ++p) {
+    int rc = orc_eval(type, n, operands, n_operands, scalars, n_scalars, ops + offs[p],
+                      args + offs[p], (int)(offs[p + 1] - offs[p]),
+                      (char*)out + (size_t)p * (size_t)n * es);
+    if (rc) return rc;
+  }
+  return ORC_E_OK;
+}
+
 /* ---- reductions ---------------------------------------------------------
  * Accumulator state so that a reduction can be fed chunk by chunk (the
  * chunked mode is bit-identical to one call over the whole array: same
