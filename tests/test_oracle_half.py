@@ -146,3 +146,59 @@ def test_generator_grid_and_overflow(etype):
     last = bits_to_float(etype, int(big.view(np.uint16)[-1]))
     # f16 overflows past 65504; bf16 has an 8-bit significand: ulp(69999) = 512, 69999 -> 137*512
     assert last == (math.inf if etype == "f16" else 70144.0)
+
+
+# ---- exhaustive: every one of the 65536 bit patterns ---------------------------
+def _round_f64_to(etype, y):
+    """Round float64 values to bf16 / f16 (nearest-even, subnormals, overflow
+    to inf), vectorised: n = rint(y / 2^q) with q the exponent of one ulp.
+    Also returns where y lies within 2^-45 |y| of a rounding midpoint."""
+    p, emin, emax = {"bf16": (8, -126, 127), "f16": (11, -14, 15)}[etype]
+    a = np.abs(y)
+    with np.errstate(all="ignore"):
+        e = np.floor(np.log2(np.where(a > 0, a, 1.0)))
+        # log2 may be off by one near powers of two: fix e so 2^e <= a < 2^(e+1)
+        e = np.where(np.exp2(e) > a, e - 1, e)
+        e = np.where(np.exp2(e + 1) <= a, e + 1, e)
+        q = np.maximum(e, emin) - (p - 1)
+        s = a / np.exp2(q)
+        frac = s - np.floor(s)
+        near = np.abs(frac - 0.5) <= 2.0 ** -45 * s
+        val = np.rint(s) * np.exp2(q)
+        val = np.where(val >= 2.0 ** (emax + 1), np.inf, val)
+        val = np.where(a == 0, 0.0, val)
+        val = np.where(np.isinf(a), np.inf, val)
+        out = np.copysign(val, y)
+        out = np.where(np.isnan(y), np.nan, out)
+    return out, near & np.isfinite(y) & (a > 0)
+
+
+@pytest.mark.parametrize("etype", HALF)
+@pytest.mark.parametrize("op", ["SQRT", "EXP", "LOG", "NEG", "ABS", "SQUARE"])
+def test_unary_ops_exhaustive(etype, op):
+    """All 65536 inputs of each unary op: the oracle equals the exact value
+    rounded once (reference: numpy f64 value rounded by _round_f64_to, and
+    mpmath at 300 bits wherever the f64 value is near a midpoint)."""
+    a = np.arange(1 << 16, dtype=np.uint32).astype(np.uint16)
+    x = np.array([bits_to_float(etype, int(b)) for b in a])
+    got = oracle.eval_program(etype, [("LOAD", 0), (op, 0)], [as_array(etype, a)]).view(np.uint16)
+    gotf = np.array([bits_to_float(etype, int(b)) for b in got])
+    if op == "NEG":
+        assert np.array_equal(got, a ^ 0x8000)
+        return
+    if op == "ABS":
+        assert np.array_equal(got, a & 0x7FFF)
+        return
+    with np.errstate(all="ignore"):
+        y = {"SQRT": np.sqrt, "EXP": np.exp, "LOG": np.log, "SQUARE": np.square}[op](x)
+    want, near = _round_f64_to(etype, y)
+    mpf = {"SQRT": mpmath.sqrt, "EXP": mpmath.exp, "LOG": mpmath.log,
+           "SQUARE": lambda v: v * v}[op]
+    for i in np.nonzero(near)[0]:
+        with mpmath.workprec(300):
+            want[i] = round_fraction(_mp_to_fraction(mpf(mpmath.mpf(float(x[i])))), etype)
+    nan = np.isnan(want)
+    assert np.array_equal(np.isnan(gotf), nan)
+    ok = nan | ((gotf == want) & (np.signbit(gotf) == np.signbit(want)))
+    bad = np.nonzero(~ok)[0]
+    assert bad.size == 0, [(hex(a[i]), x[i], gotf[i], want[i]) for i in bad[:5]]
