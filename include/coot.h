@@ -233,6 +233,41 @@ coot_status coot_partial_bytes(uint32_t kind, uint64_t len, uint64_t* bytes);
 coot_status coot_shard_range(uint64_t n, uint32_t rank, uint32_t nranks, uint64_t align,
                              uint64_t* begin, uint64_t* end);
 
+/* Communicator (one process per GPU, NCCL over NVLink /
+ * NVSwitch).  The analogue of coot_init's device selection for several GPUs.
+ *
+ * coot_comm_unique_id: one rank creates the id (COOT_COMM_ID_BYTES opaque
+ *   bytes, host memory) and the caller distributes it (e.g. a broadcast over
+ *   torch.distributed); COOT_ERR_CONFIG if NCCL cannot be loaded (libcoot
+ *   does not link it: it uses the libnccl.so.2 already loaded in the process,
+ *   else the loader's, else $COOT_NCCL_LIB).
+ * coot_comm_init: every rank binds its ctx to the communicator (collective:
+ *   all nranks ranks call it with the same id).  `shard` says how the GLOBAL
+ *   operands are split: COOT_SHARD_COLS = contiguous blocks of the global
+ *   linear index (column blocks of a Mat, row blocks of a Col; R17),
+ *   COOT_SHARD_ROWS = row blocks of a Mat (each shard a rows_r x n_cols
+ *   column-major matrix).  The ctx owns the communicator and an exchange
+ *   buffer (from ncclMemAlloc, registered as an NCCL symmetric window when the
+ *   library supports it); both are freed by coot_comm_destroy / coot_destroy.
+ * With a communicator bound, coot_reduce takes this rank's shard and returns
+ *   the GLOBAL result, identical bits on every rank: the fused kernel writes
+ *   this rank's unrounded partial, ncclAllGather collects all partials on the
+ *   ctx stream, and the combine kernel merges them in rank order 0..nranks-1
+ *   and rounds once (independent of NCCL's algorithm).  Exceptions: SUM_DIM0
+ *   with COOT_SHARD_COLS and SUM_DIM1 with COOT_SHARD_ROWS reduce along the
+ *   unsharded dimension — this rank's slice, no communication; SUM_DIM1 with
+ *   COLS / SUM_DIM0 with ROWS exchange an n_rows / n_cols vector of partials.
+ *   coot_eval never communicates (element-wise).  Like any collective, every
+ *   rank must make the matching calls in the same order with valid
+ *   arguments (a rank rejected on the host would leave the others waiting in
+ *   the all-gather).  coot_reduce_partial / coot_combine are unaffected. */
+#define COOT_COMM_ID_BYTES 128
+typedef enum { COOT_SHARD_NONE = 0, COOT_SHARD_COLS = 1, COOT_SHARD_ROWS = 2 } coot_shard_t;
+coot_status coot_comm_unique_id(void* id);
+coot_status coot_comm_init(coot_ctx* ctx, uint32_t nranks, uint32_t rank, const void* id,
+                           uint32_t shard);
+coot_status coot_comm_destroy(coot_ctx* ctx);
+
 /* In-kernel exchange (SURVEY §8(e) upgrade path / §8(f) row 4): the fused
  * reduction kernel itself publishes this rank's partial record to every
  * peer's MAILBOX over peer memory (NVLink P2P via CUDA IPC), raises a flag,
@@ -279,6 +314,17 @@ coot_status coot_reduce_exchange(coot_ctx* ctx, const coot_expr* e, uint32_t kin
 coot_status coot_fill(coot_ctx* ctx, uint32_t elem, uint32_t fill_kind, uint64_t seed,
                       uint64_t stream, uint64_t start, uint64_t count, uint64_t n_rows,
                       uint64_t k, void* out);
+
+/* Measurement only (bench.py's roofline denominators, SURVEY §8(d) "same-run
+ * stream microbenchmarks"): stream n f32 elements (n a multiple of 4, every
+ * array 16-byte aligned) from n_read (0..3) device arrays `in` into n_write
+ * (0..1) device array `out` (out[i] = sum_k in_k[i]; 1.0 when n_read == 0),
+ * nothing else.  A read-only mix needs `sink` (one device float, written only
+ * in a practically impossible case, so the loads stay live).  One launch on
+ * the ctx stream; the achieved bandwidth of each mix (1R, 2R, 3R, 1R1W, 2R1W,
+ * 3R1W) is the best the device does for that read:write ratio. */
+coot_status coot_stream_mix(coot_ctx* ctx, uint32_t n_read, uint32_t n_write, uint64_t n,
+                            const void* const* in, void* out, void* sink);
 
 /* Synchronise the ctx stream; returns COOT_ERR_DEVICE on an async fault. */
 coot_status coot_sync(coot_ctx* ctx);

@@ -97,7 +97,11 @@ _SIGS = {
     "coot_shard_range": (_i32, [_u64, _u32, _u32, _u64, ctypes.POINTER(_u64), ctypes.POINTER(_u64)]),
     "coot_fill": (_i32, [_vp, _u32, _u32, _u64, _u64, _u64, _u64, _u64, _u64, _vp]),
     "coot_sync": (_i32, [_vp]),
+    "coot_stream_mix": (_i32, [_vp, _u32, _u32, _u64, ctypes.POINTER(_vp), _vp, _vp]),
     "coot_stats": (_i32, [_vp, ctypes.POINTER(Stats)]),
+    "coot_comm_unique_id": (_i32, [_vp]),
+    "coot_comm_init": (_i32, [_vp, _u32, _u32, _vp, _u32]),
+    "coot_comm_destroy": (_i32, [_vp]),
     "coot_mailbox_create": (_i32, [_vp, ctypes.POINTER(_vp), _vp]),
     "coot_mailbox_open": (_i32, [_vp, _vp, ctypes.POINTER(_vp)]),
     "coot_mailbox_close": (_i32, [_vp, _vp]),
@@ -107,6 +111,8 @@ _SIGS = {
 }
 MAX_RANKS = 8
 IPC_HANDLE_BYTES = 64
+COMM_ID_BYTES = 128
+SHARD = {"none": 0, "cols": 1, "rows": 2}
 
 
 def _load():

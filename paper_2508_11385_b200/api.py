@@ -113,6 +113,25 @@ class Context:
                                ctypes.c_void_p(partials.data_ptr()), nparts, length,
                                ctypes.c_void_p(result.data_ptr())))
 
+    # ---- communicator (coot.h "Communicator") ---------------------------------
+    @staticmethod
+    def comm_unique_id() -> bytes:
+        """A fresh NCCL unique id (one rank creates it, every rank gets a copy)."""
+        b = ctypes.create_string_buffer(N.COMM_ID_BYTES)
+        check(lib.coot_comm_unique_id(b))
+        return b.raw
+
+    def comm_init(self, nranks: int, rank: int, uid: bytes, shard: str = "cols"):
+        """Bind this ctx to an NCCL communicator (collective over nranks ranks):
+        from then on ``reduce`` returns GLOBAL results over the ranks' shards."""
+        if shard not in N.SHARD:
+            raise CootError(5, f"contract: unknown shard kind {shard!r} (none / cols / rows)")
+        b = ctypes.create_string_buffer(bytes(uid), N.COMM_ID_BYTES)
+        check(lib.coot_comm_init(self.handle, nranks, rank, b, N.SHARD[shard]))
+
+    def comm_destroy(self):
+        check(lib.coot_comm_destroy(self.handle))
+
     # ---- in-kernel exchange (coot.h "In-kernel exchange") -------------------
     def mailbox_create(self) -> tuple[int, bytes]:
         """A zeroed mailbox on this device: (device pointer, CUDA IPC handle)."""
@@ -147,6 +166,13 @@ class Context:
              start: int = 0, n_rows: int = 1, k: int = 1):
         check(lib.coot_fill(self.handle, N.ELEM[elem_of(out)], N.FILL[kind], seed, stream, start,
                             out.numel(), n_rows, k, ctypes.c_void_p(out.data_ptr())))
+
+    def stream_mix(self, ins: list, out: torch.Tensor | None, n: int, sink: torch.Tensor):
+        """Measurement kernel (coot_stream_mix): stream n f32 from `ins` into `out`."""
+        arr = (ctypes.c_void_p * max(1, len(ins)))(*[t.data_ptr() for t in ins])
+        check(lib.coot_stream_mix(self.handle, len(ins), 1 if out is not None else 0, n, arr,
+                                  ctypes.c_void_p(out.data_ptr() if out is not None else 0),
+                                  ctypes.c_void_p(sink.data_ptr())))
 
     def sync(self):
         check(lib.coot_sync(self.handle))

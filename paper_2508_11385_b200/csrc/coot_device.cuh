@@ -7,8 +7,8 @@
 //  * every node rounds to eT, no FMA contraction: explicit __f*_rn / __d*_rn
 //    intrinsics (and the build uses -fmad=false, no FTZ, IEEE div/sqrt), so
 //    + - * / sqrt are bit-identical to the eager oracle;
-//  * f32 EXP/LOG are computed in f64 and rounded once (correctly rounded
-//    except in ~2^-28 of cases); f64 EXP/LOG use CUDA exp/log (<= 1 ulp);
+//  * EXP/LOG are correctly rounded in every float type (coot_crmath.cuh: a
+//    fast phase with a rounding test, a double-double accurate phase);
 //  * f32 reductions: 16-byte unit (4 elements) summed pairwise in f32, then
 //    accumulated in f64; the final value is rounded once to eT;
 //  * integers: modular (u64 accumulator, truncated at the end).
@@ -19,6 +19,7 @@
 #include <stdint.h>
 
 #include "../../include/coot.h"
+#include "coot_crmath.cuh"
 
 namespace coot {
 
@@ -413,44 +414,8 @@ __host__ __device__ constexpr bool op_legal(int op) {
                            op == COOT_OP_DIV);
 }
 
-// ---- f32 exp evaluated in f64 (R6) -------------------------------------------
-// e^x = 2^m * 2^(j/64) * e^r with k = rint(x * 64/ln2) = 64m + j and
-// r = x - k*ln2/64 (Cody-Waite, ln2/64 split hi/lo; |r| <= ln2/128 = 0.0054).
-// e^r - 1 by a degree-6 Taylor polynomial (truncation < 3e-20), 2^(j/64) from a
-// correctly rounded table: total relative error < 2^-52 before the single
-// rounding to f32, so the f32 result is the correctly rounded one except when
-// e^x lies within ~2^-52 (relative) of an f32 rounding boundary.  About 12
-// FP64 operations per element (half the generic f64 exp).
-static __device__ const double kExp2Tab[64] = {
-#include "exp2_table.inc"
-};
-
-__device__ __forceinline__ double exp_f64_of_f32(float xf) {
-  const float xc = fminf(fmaxf(xf, -104.0f), 89.0f);  // e^-104 < 2^-150 -> 0; e^89 -> inf
-  const double x = (double)xc;
-  const double kShift = 0x1.8p52;                            // 1.5 * 2^52: rint trick
-  const double ks = __fma_rn(x, 0x1.71547652b82fep+6, kShift);  // x * 64/ln2 + shift
-  const double k = __dsub_rn(ks, kShift);
-  const int ki = (int)__double2loint(ks);  // k as a 32-bit integer
-  // ln2/64 = C1 + C2 (C1 = RN(ln2/64)); the FMA forms k*C1 exactly
-  const double r = __fma_rn(-k, 0x1.62e42fefa39efp-7, x);
-  const double rr = __fma_rn(-k, 0x1.abc9e3b39803fp-62, r);
-  double p = __fma_rn(rr, 1.0 / 720.0, 1.0 / 120.0);
-  p = __fma_rn(p, rr, 1.0 / 24.0);
-  p = __fma_rn(p, rr, 1.0 / 6.0);
-  p = __fma_rn(p, rr, 0.5);
-  p = __fma_rn(p, rr, 1.0);
-  p = __dmul_rn(p, rr);  // e^r - 1
-  const double t = __ldg(&kExp2Tab[ki & 63]);
-  double y = __fma_rn(t, p, t);  // 2^(j/64) * e^r
-  y = __longlong_as_double(__double_as_longlong(y) + ((long long)(ki >> 6) << 52));
-  return (xf != xf) ? (double)xf : y;  // NaN passes through
-}
-
-// f32 / bf16 / f16 EXP: the f64 value above, rounded once to the format.
-__device__ __forceinline__ float exp_f32_via_f64(float xf) {
-  return __double2float_rn(exp_f64_of_f32(xf));
-}
+// ---- EXP / LOG (R6): correctly rounded, coot_crmath.cuh ----------------------
+using crm::exp_f64_of_f32;  // f32 e^x as a double within 2^-51 (the 16-bit types' fallback)
 
 // ---- element semantics ------------------------------------------------------
 template <int OP>
@@ -459,14 +424,13 @@ __device__ __forceinline__ float un(float a) {
   else if constexpr (OP == COOT_OP_ABS) return fabsf(a);
   else if constexpr (OP == COOT_OP_SQUARE) return __fmul_rn(a, a);
   else if constexpr (OP == COOT_OP_SQRT) return __fsqrt_rn(a);
-  // f32 EXP/LOG are evaluated in f64 (B200 runs FP64 at half the FP32 rate)
-  // and rounded once: the f64 result is within 1 ulp(f64), so the f32 result
-  // is the correctly rounded one except when exp(x)/log(x) lies within
-  // ~2^-52 relative of an f32 rounding boundary (R6).  This keeps
-  // composed expressions bit-identical to the correctly-rounded oracle, where
-  // expf/logf (<= 2 / 1 ulp) would let later nodes amplify the difference.
-  else if constexpr (OP == COOT_OP_EXP) return exp_f32_via_f64(a);
-  else if constexpr (OP == COOT_OP_LOG) return __double2float_rn(log((double)a));
+  // f32 EXP/LOG are correctly rounded (R6, coot_crmath.cuh): evaluated in
+  // f64 and rounded once when that provably decides the f32 result, else by
+  // the double-double accurate phase.  This keeps composed expressions
+  // bit-identical to the correctly rounded oracle, where expf/logf (<= 2 / 1
+  // ulp) would let later nodes amplify the difference.
+  else if constexpr (OP == COOT_OP_EXP) return crm::cr_expf(a);
+  else if constexpr (OP == COOT_OP_LOG) return crm::cr_logf(a);
   else return a;
 }
 template <int OP>
@@ -475,8 +439,8 @@ __device__ __forceinline__ double un(double a) {
   else if constexpr (OP == COOT_OP_ABS) return fabs(a);
   else if constexpr (OP == COOT_OP_SQUARE) return __dmul_rn(a, a);
   else if constexpr (OP == COOT_OP_SQRT) return __dsqrt_rn(a);
-  else if constexpr (OP == COOT_OP_EXP) return exp(a);
-  else if constexpr (OP == COOT_OP_LOG) return log(a);
+  else if constexpr (OP == COOT_OP_EXP) return crm::cr_exp(a);  // correctly rounded (R6)
+  else if constexpr (OP == COOT_OP_LOG) return crm::cr_log(a);
   else return a;
 }
 // bf16 / f16 EXP / LOG (R24): the f32 expf / logf result (CUDA math library:

@@ -53,4 +53,9 @@ cudaError_t launch_fill_t(uint32_t kind, unsigned long long seed, unsigned long 
                           unsigned long long n_rows, unsigned long long k, void* out,
                           unsigned grid, cudaStream_t s);
 
+// stream microbenchmark (coot_stream.cu): units of 16 bytes (4 x f32)
+cudaError_t launch_stream_mix(uint32_t n_read, uint32_t n_write, unsigned long long units,
+                              const void* const* in, void* out, void* sink, int sm_count,
+                              cudaStream_t s);
+
 }  // namespace coot

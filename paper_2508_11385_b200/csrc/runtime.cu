@@ -8,6 +8,7 @@
 // B200 analogue of "the minimal set of calls".  All validation is
 // host-only and happens before anything is enqueued.
 #include <cuda_runtime.h>
+#include <dlfcn.h>
 
 #include <algorithm>
 #include <cstdarg>
@@ -21,6 +22,65 @@
 #include "coot_internal.h"
 
 using coot::u64;
+
+// ---- NCCL, loaded at first use (coot_comm_*) ---------------------------------
+// The types and the calls below are NCCL's public C API as declared in nccl.h
+// (2.27 / 2.28: ncclUniqueId is 128 bytes, ncclResult_t / ncclDataType_t are
+// int-sized enums, ncclUint8 = 1, NCCL_WIN_COLL_SYMMETRIC = 1).  The library
+// is the one already loaded in the process (torch's), else libnccl.so.2 from
+// the loader path, else $COOT_NCCL_LIB — libcoot does not link NCCL, so a
+// single-GPU user never needs it.
+namespace nccl {
+typedef struct ncclComm* comm_t;
+typedef struct ncclWindow_vidmem* window_t;
+typedef struct {
+  char internal[128];
+} unique_id;
+typedef int result_t;
+constexpr int kUint8 = 1;
+constexpr int kWinCollSymmetric = 1;
+struct Api {
+  bool tried = false, ok = false;
+  std::string why;
+  result_t (*GetUniqueId)(unique_id*) = nullptr;
+  result_t (*CommInitRank)(comm_t*, int, unique_id, int) = nullptr;
+  result_t (*CommDestroy)(comm_t) = nullptr;
+  result_t (*AllGather)(const void*, void*, size_t, int, comm_t, cudaStream_t) = nullptr;
+  const char* (*GetErrorString)(result_t) = nullptr;
+  result_t (*MemAlloc)(void**, size_t) = nullptr;  // optional (>= 2.19)
+  result_t (*MemFree)(void*) = nullptr;
+  result_t (*CommWindowRegister)(comm_t, void*, size_t, window_t*, int) = nullptr;  // >= 2.27
+  result_t (*CommWindowDeregister)(comm_t, window_t) = nullptr;
+};
+Api& api() {
+  static Api a;
+  if (a.tried) return a;
+  a.tried = true;
+  void* h = nullptr;
+  if (const char* env = getenv("COOT_NCCL_LIB")) h = dlopen(env, RTLD_NOW | RTLD_LOCAL);
+  if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+  if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_LOCAL);
+  if (!h) {
+    a.why = dlerror() ? dlerror() : "libnccl.so.2 not found";
+    return a;
+  }
+  auto sym = [&](const char* n) { return dlsym(h, n); };
+  a.GetUniqueId = reinterpret_cast<result_t (*)(unique_id*)>(sym("ncclGetUniqueId"));
+  a.CommInitRank = reinterpret_cast<result_t (*)(comm_t*, int, unique_id, int)>(sym("ncclCommInitRank"));
+  a.CommDestroy = reinterpret_cast<result_t (*)(comm_t)>(sym("ncclCommDestroy"));
+  a.AllGather = reinterpret_cast<result_t (*)(const void*, void*, size_t, int, comm_t, cudaStream_t)>(
+      sym("ncclAllGather"));
+  a.GetErrorString = reinterpret_cast<const char* (*)(result_t)>(sym("ncclGetErrorString"));
+  a.MemAlloc = reinterpret_cast<result_t (*)(void**, size_t)>(sym("ncclMemAlloc"));
+  a.MemFree = reinterpret_cast<result_t (*)(void*)>(sym("ncclMemFree"));
+  a.CommWindowRegister = reinterpret_cast<result_t (*)(comm_t, void*, size_t, window_t*, int)>(
+      sym("ncclCommWindowRegister"));
+  a.CommWindowDeregister = reinterpret_cast<result_t (*)(comm_t, window_t)>(sym("ncclCommWindowDeregister"));
+  a.ok = a.GetUniqueId && a.CommInitRank && a.CommDestroy && a.AllGather && a.GetErrorString;
+  if (!a.ok) a.why = "libnccl.so.2 lacks a required symbol";
+  return a;
+}
+}  // namespace nccl
 
 struct coot_ctx {
   int device = 0;
@@ -50,6 +110,14 @@ struct coot_ctx {
   bool log = false;
   const coot::Exchange* pending_ex = nullptr;  // set by coot_reduce_exchange for one call
   cudaEvent_t handoff = nullptr;  // orders a new stream after the old one (coot_set_stream)
+  // communicator (coot_comm_init): partial -> all-gather -> rank-order combine
+  nccl::comm_t comm = nullptr;
+  int nranks = 1, rank = 0;
+  uint32_t shard = COOT_SHARD_NONE;
+  void* comm_buf = nullptr;        // [send: S bytes][recv: nranks * S bytes]
+  size_t comm_buf_bytes = 0;
+  bool comm_buf_nccl = false;      // from ncclMemAlloc (else cudaMalloc)
+  nccl::window_t comm_win = nullptr;  // symmetric window over comm_buf, if registered
 };
 
 // Whether the TMA producer should sleep (rather than poll) while the ring is
@@ -1040,6 +1108,7 @@ coot_status coot_destroy(coot_ctx* ctx) {
   if (!ctx) return ok();
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
+  if (ctx->comm) coot_comm_destroy(ctx);
   cudaFree(ctx->recs);
   cudaFree(ctx->ticket);
   cudaFree(ctx->dim_part);
@@ -1078,8 +1147,12 @@ coot_status coot_eval_view(coot_ctx* ctx, const coot_expr* e, const coot_operand
   return eval_common(ctx, e, out);
 }
 
+static coot_status reduce_comm(coot_ctx* ctx, const coot_expr* e, uint32_t kind, void* result,
+                               void* out_or_null);
+
 coot_status coot_reduce(coot_ctx* ctx, const coot_expr* e, uint32_t kind, void* result,
                         void* out_or_null) {
+  if (ctx && ctx->comm) return reduce_comm(ctx, e, kind, result, out_or_null);
   return reduce_common(ctx, e, kind, result, out_or_null, coot::FINAL_ROUND);
 }
 
@@ -1211,6 +1284,143 @@ coot_status coot_combine(coot_ctx* ctx, uint32_t elem, uint32_t kind, const void
   return ok();
 }
 
+// ---- communicator -------------------------------------------------------------
+static coot_status nccl_fail(nccl::result_t r, const char* what) {
+  return fail(COOT_ERR_DEVICE, "device: %s: NCCL error %d (%s)", what, r,
+              nccl::api().GetErrorString ? nccl::api().GetErrorString(r) : "?");
+}
+
+static void comm_free_buf(coot_ctx* ctx) {
+  nccl::Api& a = nccl::api();
+  if (ctx->comm_win && a.CommWindowDeregister) a.CommWindowDeregister(ctx->comm, ctx->comm_win);
+  ctx->comm_win = nullptr;
+  if (ctx->comm_buf) {
+    if (ctx->comm_buf_nccl) a.MemFree(ctx->comm_buf);
+    else cudaFree(ctx->comm_buf);
+  }
+  ctx->comm_buf = nullptr;
+  ctx->comm_buf_bytes = 0;
+}
+
+// The exchange buffer (send + nranks receive slots of `slot` bytes each).
+// Every rank grows it at the same call (the slot size is a function of the
+// call's kind and global shape), so the collective window registration
+// matches across ranks.
+static coot_status comm_reserve(coot_ctx* ctx, size_t slot) {
+  const size_t need = slot * (size_t)(ctx->nranks + 1);
+  if (need <= ctx->comm_buf_bytes) return ok();
+  cudaError_t ce = cudaStreamSynchronize(ctx->stream);  // the old buffer may be in flight
+  if (ce != cudaSuccess) return cuda_fail(ce, "cudaStreamSynchronize");
+  comm_free_buf(ctx);
+  size_t bytes = 64u << 10;
+  while (bytes < need) bytes *= 2;
+  nccl::Api& a = nccl::api();
+  if (a.MemAlloc && a.MemFree && a.MemAlloc(&ctx->comm_buf, bytes) == 0) {
+    ctx->comm_buf_nccl = true;
+  } else {
+    ctx->comm_buf_nccl = false;
+    ce = cudaMalloc(&ctx->comm_buf, bytes);
+    if (ce != cudaSuccess) {
+      ctx->comm_buf = nullptr;
+      return fail(COOT_ERR_RESOURCE, "resource: cannot allocate %zu bytes of exchange buffer", bytes);
+    }
+  }
+  ctx->comm_buf_bytes = bytes;
+  // symmetric window: lets NCCL use its low-latency symmetric-memory kernels
+  // for the all-gather of the partials (SURVEY §8(e) upgrade path 1)
+  if (ctx->comm_buf_nccl && a.CommWindowRegister &&
+      a.CommWindowRegister(ctx->comm, ctx->comm_buf, bytes, &ctx->comm_win,
+                           nccl::kWinCollSymmetric) != 0)
+    ctx->comm_win = nullptr;
+  return ok();
+}
+
+// coot_reduce with a communicator: this rank's unrounded partial (the fused
+// kernel, FINAL_PARTIAL), an all-gather of the partials, and the rank-order
+// combine kernel — all on the ctx stream; every rank ends with the same bits.
+// SUM_DIM along the unsharded dimension needs no exchange.
+static coot_status reduce_comm(coot_ctx* ctx, const coot_expr* e, uint32_t kind, void* result,
+                               void* out_or_null) {
+  if (!e) return fail(COOT_ERR_CONTRACT, "contract: expression descriptor is NULL");
+  const bool dim = kind == COOT_RED_SUM_DIM0 || kind == COOT_RED_SUM_DIM1;
+  u64 len = 1;
+  if (dim) {
+    const bool exchange = (kind == COOT_RED_SUM_DIM1 && ctx->shard == COOT_SHARD_COLS) ||
+                          (kind == COOT_RED_SUM_DIM0 && ctx->shard == COOT_SHARD_ROWS);
+    if (!exchange) return reduce_common(ctx, e, kind, result, out_or_null, coot::FINAL_ROUND);
+    len = kind == COOT_RED_SUM_DIM1 ? e->n_rows : e->n_cols;
+  }
+  const size_t slot = dim ? (size_t)len * 8 : (size_t)COOT_PARTIAL_BYTES;
+  coot_status st = comm_reserve(ctx, slot);
+  if (st != COOT_OK) return st;
+  char* send = static_cast<char*>(ctx->comm_buf);
+  char* recv = send + slot;
+  st = reduce_common(ctx, e, kind, send, out_or_null, coot::FINAL_PARTIAL);
+  if (st != COOT_OK) return st;
+  const nccl::result_t r = nccl::api().AllGather(send, recv, slot, nccl::kUint8, ctx->comm, ctx->stream);
+  if (r != 0) return nccl_fail(r, "ncclAllGather");
+  return coot_combine(ctx, e->elem, kind, recv, (uint32_t)ctx->nranks, len, result);
+}
+
+coot_status coot_comm_unique_id(void* id) {
+  if (!id) return fail(COOT_ERR_CONTRACT, "contract: id is NULL");
+  nccl::Api& a = nccl::api();
+  if (!a.ok) return fail(COOT_ERR_CONFIG, "configuration: NCCL unavailable (%s)", a.why.c_str());
+  nccl::unique_id u;
+  const nccl::result_t r = a.GetUniqueId(&u);
+  if (r != 0) return nccl_fail(r, "ncclGetUniqueId");
+  memcpy(id, &u, sizeof u);
+  return ok();
+}
+
+coot_status coot_comm_init(coot_ctx* ctx, uint32_t nranks, uint32_t rank, const void* id,
+                           uint32_t shard) {
+  coot_status st = check_ctx(ctx);
+  if (st != COOT_OK) return st;
+  if (!id) return fail(COOT_ERR_CONTRACT, "contract: id is NULL");
+  if (nranks == 0 || rank >= nranks)
+    return fail(COOT_ERR_CONFIG, "configuration: rank %u of %u", rank, nranks);
+  if (shard > COOT_SHARD_ROWS) return fail(COOT_ERR_CONTRACT, "contract: unknown shard kind %u", shard);
+  if (ctx->comm) return fail(COOT_ERR_CONFIG, "configuration: ctx already has a communicator");
+  nccl::Api& a = nccl::api();
+  if (!a.ok) return fail(COOT_ERR_CONFIG, "configuration: NCCL unavailable (%s)", a.why.c_str());
+  st = bind_device(ctx);
+  if (st != COOT_OK) return st;
+  nccl::unique_id u;
+  memcpy(&u, id, sizeof u);
+  nccl::comm_t c = nullptr;
+  const nccl::result_t r = a.CommInitRank(&c, (int)nranks, u, (int)rank);
+  if (r != 0) return nccl_fail(r, "ncclCommInitRank");
+  ctx->comm = c;
+  ctx->nranks = (int)nranks;
+  ctx->rank = (int)rank;
+  ctx->shard = shard;
+  st = comm_reserve(ctx, COOT_PARTIAL_BYTES);
+  if (st != COOT_OK) {
+    a.CommDestroy(c);
+    ctx->comm = nullptr;
+    ctx->nranks = 1;
+    ctx->rank = 0;
+  }
+  return st;
+}
+
+coot_status coot_comm_destroy(coot_ctx* ctx) {
+  coot_status st = check_ctx(ctx);
+  if (st != COOT_OK) return st;
+  if (!ctx->comm) return ok();
+  st = bind_device(ctx);
+  if (st != COOT_OK) return st;
+  cudaStreamSynchronize(ctx->stream);
+  comm_free_buf(ctx);
+  nccl::api().CommDestroy(ctx->comm);
+  ctx->comm = nullptr;
+  ctx->nranks = 1;
+  ctx->rank = 0;
+  ctx->shard = COOT_SHARD_NONE;
+  return ok();
+}
+
 coot_status coot_shard_range(uint64_t n, uint32_t rank, uint32_t nranks, uint64_t align,
                              uint64_t* begin, uint64_t* end) {
   if (!begin || !end) return fail(COOT_ERR_CONTRACT, "contract: NULL begin/end");
@@ -1255,6 +1465,33 @@ coot_status coot_fill(coot_ctx* ctx, uint32_t elem, uint32_t fill_kind, uint64_t
   ctx->stats.launches++;
   ctx->stats.last_path = -3;
   ctx->stats.last_grid = grid;
+  return ok();
+}
+
+coot_status coot_stream_mix(coot_ctx* ctx, uint32_t n_read, uint32_t n_write, uint64_t n,
+                            const void* const* in, void* out, void* sink) {
+  coot_status st = check_ctx(ctx);
+  if (st != COOT_OK) return st;
+  if (n_read > 3 || n_write > 1 || n_read + n_write == 0)
+    return fail(COOT_ERR_BOUNDS, "bounds: stream mix %uR%uW (allowed 0..3 reads, 0..1 writes)",
+                n_read, n_write);
+  if (n % 4) return fail(COOT_ERR_CONTRACT, "contract: stream mix length %llu is not a multiple of 4",
+                         (unsigned long long)n);
+  if (n == 0) return ok();
+  for (uint32_t k = 0; k < n_read; ++k)
+    if (!in || !in[k] || reinterpret_cast<uintptr_t>(in[k]) % 16)
+      return fail(COOT_ERR_CONTRACT, "contract: stream input %u is NULL or not 16-byte aligned", k);
+  if (n_write && (!out || reinterpret_cast<uintptr_t>(out) % 16))
+    return fail(COOT_ERR_CONTRACT, "contract: stream output is NULL or not 16-byte aligned");
+  if (!n_write && !sink) return fail(COOT_ERR_CONTRACT, "contract: a read-only mix needs a sink");
+  st = bind_device(ctx);
+  if (st != COOT_OK) return st;
+  cudaError_t ce = coot::launch_stream_mix(n_read, n_write, n / 4, in, out, sink, ctx->sm_count,
+                                           ctx->stream);
+  if (ce != cudaSuccess) return cuda_fail(ce, "stream kernel launch");
+  ctx->stats.launches++;
+  ctx->stats.last_path = -3;
+  ctx->stats.last_alg_bytes = n * 4 * (n_read + n_write);
   return ok();
 }
 

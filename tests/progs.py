@@ -107,7 +107,7 @@ def ulp_distance(got: np.ndarray, want: np.ndarray) -> np.ndarray:
     return d
 
 
-def assert_elementwise(got, want, etype, max_ulp=2):
+def assert_elementwise(got, want, etype, max_ulp=0):
     got, want = np.asarray(got), np.asarray(want)
     assert got.shape == want.shape, (got.shape, want.shape)
     if got.size == 0:

@@ -32,3 +32,21 @@ def test_reference_arm_json_line():
     e = d["e2e"]
     assert e["value"] == d["value"] and e["unit"] == d["unit"]
     assert e["h2d_bytes_per_step"] == 0 and e["d2h_bytes_per_step"] == 0
+
+
+def test_gpus_flag_self_launch_refuses_without_devices():
+    """--gpus N > 1 outside torchrun launches N ranks itself; with fewer visible
+    GPUs it must fail loudly instead of timing one rank under n_gpus: N."""
+    env = dict(os.environ, CUDA_VISIBLE_DEVICES="")
+    env.pop("WORLD_SIZE", None)
+    p = subprocess.run([sys.executable, "bench.py", "--gpus", "2", "--steps", "3"], cwd=ROOT,
+                       env=env, capture_output=True, text=True, timeout=300)
+    assert p.returncode == 2 and "--gpus 2" in p.stderr, (p.returncode, p.stderr[-500:])
+    assert p.stdout.strip() == ""
+
+
+def test_world_size_must_match_gpus_flag():
+    env = dict(os.environ, CUDA_VISIBLE_DEVICES="", WORLD_SIZE="1", RANK="0", LOCAL_RANK="0")
+    p = subprocess.run([sys.executable, "bench.py", "--gpus", "2", "--steps", "3"], cwd=ROOT,
+                       env=env, capture_output=True, text=True, timeout=300)
+    assert p.returncode == 2 and "WORLD_SIZE=1" in p.stderr, (p.returncode, p.stderr[-500:])

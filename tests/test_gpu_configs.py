@@ -57,7 +57,7 @@ def test_c2_full(ctx, store):
                                 scalars=[3.0], kind="ACCU", want_out=store)
     assert_reduction(r[0].item(), acc, "f32", "ACCU")
     if store:
-        assert_elementwise(to_host(Z, "f32"), z, "f32", max_ulp=2)
+        assert_elementwise(to_host(Z, "f32"), z, "f32", max_ulp=0)
     # statistical wiring check: E[Z] = Ei(1) - gamma + 1.5 = 2.8179 (sd 9.25e-5 at 1e8)
     assert abs(r[0].item() / (m * n) - 2.8179021514544039) < 1e-3
 

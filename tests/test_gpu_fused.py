@@ -10,7 +10,7 @@ import torch
 import oracle
 from gpu_util import TORCH, empty_dev, requires_gpu, to_dev, to_host
 from progs import (ALL, CATALOG, C2, FLOATS, INTS, P, assert_elementwise, assert_reduction,
-                   has_transcendental, legal, n_operands, n_scalars, random_program)
+                   legal, n_operands, n_scalars, random_program)
 
 pytestmark = [pytest.mark.gpu, requires_gpu]
 
@@ -90,7 +90,7 @@ def test_catalog_programs_eval_and_reduce(ctx, etype, cat):
     want = oracle.eval_program(etype, prog, ops, sc)
     got = run_eval(ctx, etype, prog, ops, sc)
     assert ctx.stats()["last_path"] == cat
-    assert_elementwise(got, want, etype, max_ulp=2 if has_transcendental(prog) else 0)
+    assert_elementwise(got, want, etype, max_ulp=0)
     kinds = ["ACCU", "MIN", "MAX", "MINMAX"] + (["NORM2"] if etype in FLOATS else [])
     for kind in kinds:
         r = run_reduce(ctx, etype, prog, ops, sc, kind)
@@ -110,16 +110,8 @@ def test_interpreter_random_programs(ctx, etype):
         sc = SCAL[etype][:2]
         want = oracle.eval_program(etype, prog, ops, sc)
         got = run_eval(ctx, etype, prog, ops, sc)
-        if etype == "f64" and has_transcendental(prog):
-            # f64 exp/log are <= 1 ulp, not correctly rounded (R6): later
-            # nodes may amplify that, so composed f64 programs are held to 1e-12 rel.
-            g, w = got.astype(np.float64), want.astype(np.float64)
-            fin = np.isfinite(w)
-            assert np.array_equal(np.isnan(g), np.isnan(w))
-            rel = np.abs(g[fin] - w[fin]) / np.maximum(np.abs(w[fin]), 1e-300)
-            assert rel.size == 0 or rel.max() <= 1e-12, (prog, rel.max())
-        else:
-            assert_elementwise(got, want, etype, max_ulp=2 if has_transcendental(prog) else 0)
+        # every node is correctly rounded (EXP / LOG included, R6): bit-exact
+        assert_elementwise(got, want, etype, max_ulp=0)
         if np.all(np.isfinite(want.astype(np.float64))) or etype in INTS:
             kind = "ACCU" if trial % 2 else "MINMAX"
             r = run_reduce(ctx, etype, prog, ops, sc, kind)
@@ -351,7 +343,7 @@ def test_ldg_driver_parity(ctx_ldg, etype):
         sc = SCAL[etype][:n_scalars(prog)]
         want = oracle.eval_program(etype, prog, ops, sc)
         r, got = run_reduce(ctx_ldg, etype, prog, ops, sc, "ACCU", with_out=True)
-        assert_elementwise(got, want, etype, max_ulp=2 if has_transcendental(prog) else 0)
+        assert_elementwise(got, want, etype, max_ulp=0)
         assert_reduction(r, oracle_reduce(etype, "ACCU", want), etype, "ACCU", abs_scale(want))
     rng = random.Random(77)
     for trial in range(10):
@@ -359,9 +351,7 @@ def test_ldg_driver_parity(ctx_ldg, etype):
         ops = make_inputs(etype, 4001, n_operands(prog), seed=trial)
         want = oracle.eval_program(etype, prog, ops, SCAL[etype][:2])
         got = run_eval(ctx_ldg, etype, prog, ops, SCAL[etype][:2])
-        if etype == "f64" and has_transcendental(prog):
-            continue
-        assert_elementwise(got, want, etype, max_ulp=2 if has_transcendental(prog) else 0)
+        assert_elementwise(got, want, etype, max_ulp=0)
 
 
 # Fused-operand dispatch (runtime.cu fill_program): every ADD / SUB / MUL whose

@@ -31,6 +31,10 @@ WL = {
     "axpy_interp_2p30": ("f32", 1 << 30, 1, "S0 L0 MUL L1 ADD", [2.5], "ACCU", True, True),
     "poly_interp_2p30": ("f32", 1 << 30, 1, "L0 L1 MUL L2 ADD L0 MUL S0 SUB ABS SQRT", [0.5], "ACCU", True, True),
     "f64_c2_interp_2p29": ("f64", 1 << 29, 1, "L0 L1 MUL EXP S0 L2 MUL ADD", [3.0], "ACCU", False, True),
+    "f64_c2_2p29": ("f64", 1 << 29, 1, "L0 L1 MUL EXP S0 L2 MUL ADD", [3.0], "ACCU", False, False),
+    "f64_log_2p29": ("f64", 1 << 29, 1, "L0 LOG L1 ADD", [], "ACCU", False, False),
+    "f64_log_interp_2p29": ("f64", 1 << 29, 1, "L0 LOG L1 ADD", [], "ACCU", False, True),
+    "f32_log_interp_2p30": ("f32", 1 << 30, 1, "L0 LOG L1 ADD", [], "ACCU", False, True),
     "hl_c2_2p30": ("f32", 1 << 30, 1, "L0 L1 MUL EXP S0 L2 MUL ADD", [3.0], "ACCU", False, False),
     "axpy_accu_2p30": ("f32", 1 << 30, 1, "S0 L0 MUL L1 ADD", [2.5], "ACCU", True, False),
     "axpy_reduce_2p30": ("f32", 1 << 30, 1, "S0 L0 MUL L1 ADD", [2.5], "ACCU", False, False),
