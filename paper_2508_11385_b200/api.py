@@ -169,7 +169,7 @@ class Context:
 
     def stream_mix(self, ins: list, out: torch.Tensor | None, n: int, sink: torch.Tensor):
         """Measurement kernel (coot_stream_mix): stream n f32 from `ins` into `out`."""
-        arr = (ctypes.c_void_p * max(1, len(ins)))(*[t.data_ptr() for t in ins])
+        arr = (ctypes.c_void_p * builtins.max(1, len(ins)))(*[t.data_ptr() for t in ins])
         check(lib.coot_stream_mix(self.handle, len(ins), 1 if out is not None else 0, n, arr,
                                   ctypes.c_void_p(out.data_ptr() if out is not None else 0),
                                   ctypes.c_void_p(sink.data_ptr())))

@@ -49,7 +49,7 @@ namespace crm {
 namespace dev {
 #define CRM_TABLE static __device__ const
 #include "crmath_tables.inc"
-static __device__ const double kExp2Tab[64] = {
+static __device__ const double kExp2Tab[128] = {
 #include "exp2_table.inc"
 };
 #undef CRM_TABLE
@@ -58,7 +58,7 @@ static __device__ const double kExp2Tab[64] = {
 namespace host {
 #define CRM_TABLE static const
 #include "crmath_tables.inc"
-static const double kExp2Tab[64] = {
+static const double kExp2Tab[128] = {
 #include "exp2_table.inc"
 };
 #undef CRM_TABLE
@@ -138,14 +138,20 @@ CRM_HD bool f64_decided(dd y, double c) { return y.hi + y.lo * c == y.hi; }
 
 // f32 rounding of a double y known to within `margin` double ulps: decided
 // unless y lies within margin ulps of an f32 rounding midpoint (the low 29
-// mantissa bits 1000...0), or y is below the f32 normal range (there the f32
-// grid is coarser than bit 29).  0, inf and NaN are decided.
+// mantissa bits 1000...0), or 0 < |y| < 2^-126 (below the f32 normal range
+// the f32 grid is coarser than bit 29).  0, inf and the canonical NaN have
+// zero low bits and are decided.  Integer-only, branch-free (it runs once per
+// element on the hot path).
+CRM_HD bool f32_mid_clear(double y, uint32_t margin) {
+  const uint32_t lo = (uint32_t)bits_of(y) & 0x1fffffffu;
+  return ((lo + (0x10000000u + margin)) & 0x1fffffffu) > 2 * margin;
+}
 CRM_HD bool f32_decided(double y, uint32_t margin) {
-  const double a = fabs(y);
-  if (!(a < INFINITY) || a == 0) return true;
-  if (a < 0x1p-126) return false;
-  const uint32_t low = (uint32_t)bits_of(y) & 0x1fffffffu;
-  return ((low + (0x10000000u + margin)) & 0x1fffffffu) > 2 * margin;
+  const uint64_t u = bits_of(y);
+  const uint32_t hi = (uint32_t)(u >> 32) & 0x7fffffffu;
+  const uint32_t lo = (uint32_t)u & 0x1fffffffu;
+  const bool clear = ((lo + (0x10000000u + margin)) & 0x1fffffffu) > 2 * margin;
+  return clear && (hi - 1u >= 0x380fffffu);  // hi == 0 (zero) or |y| >= 2^-126
 }
 
 // f32 RN(hi + lo) for a normalised double-double: RN(hi) unless hi is itself
@@ -166,15 +172,18 @@ CRM_HD float f32_of_dd(dd y) {
 
 // ---- exp -----------------------------------------------------------------------
 // Fast phase: e^x = 2^m (hi + lo), relative error < 2^-67 (degree-6 Taylor on
-// |r| <= 2^-8.5: truncation < 2^-71.8; the rest are double roundings of terms
-// below 2^-17 relative).
+// |r| <= 2^-8.5: truncation < 2^-71.8; r to < 2^-78 (k ln2/128 to 2^-82,
+// Fast2Sum of s - t exact unless |s| < |t| < 2^-26, then off by < 2^-79); the
+// rest are double roundings of terms below 2^-17 relative).  ~30 FP64 ops.
 CRM_HD dd exp_fast(double x, int* m) {
-  const double kd = rint(x * kExpInvL);
-  const int k = (int)kd;
-  const double s = x - kd * kExpL1;  // exact: kd * L1 fits 53 bits, s in [2^-43, 2^-8]
-  const double t = kd * kExpL2;      // |t| < 2^-26; rounding < 2^-79
-  const dd r = two_sum(s, -t);       // r = r.hi + r.lo (exact sum of s - t)
-  const double rh = r.hi, rl = r.lo - kd * kExpL3;
+  const double kShift = 0x1.8p52;  // rint trick: k in the low bits of ks
+  const double ks = fma(x, kExpInvL, kShift);
+  const double kd = ks - kShift;
+  const int k = (int)(bits_of(ks) & 0xffffffffu);
+  const double s = fma(-kd, kExpL1, x);  // exact: kd * L1 fits 53 bits, s in [2^-43, 2^-8]
+  const double t = kd * kExpL2;          // |t| < 2^-26; rounding < 2^-79 (kd L3 < 2^-82: dropped)
+  const double rh = s - t;
+  const double rl = (s - rh) - t;
   double P = fma(rh, 1.0 / 720, 1.0 / 120);
   P = fma(P, rh, 1.0 / 24);
   P = fma(P, rh, 1.0 / 6);
@@ -189,6 +198,13 @@ CRM_HD dd exp_fast(double x, int* m) {
   y.lo += p.lo + fma(Th, qlo, fma(Tl, rh, Tl));
   *m = k >> 7;
   return fast_two_sum(y.hi, y.lo);
+}
+
+// v * 2^m by an add to the exponent field (v normal, the result normal)
+CRM_HD double scale_exp(double v, int m) {
+  const uint64_t u = bits_of(v);
+  return double_of(((uint64_t)((uint32_t)(u >> 32) + ((uint32_t)m << 20)) << 32) |
+                   (u & 0xffffffffu));
 }
 
 // Accurate phase: relative error < 2^-100 (dd Taylor to degree 10 on |r| <=
@@ -264,6 +280,20 @@ CRM_SLOW double exp_f64_slow(double x) {
   return scale_normal(y.hi, m);
 }
 
+// Vectorisable fast phase of cr_exp: straight-line code for any x (clamped
+// into the ordinary range); `ok` is false when x needs a special path (NaN,
+// |x| < 2^-26, results outside [2^-1021, 2^1024)) or the rounding test fails
+// — then cr_exp(x) (the slow, branchy version) must be used.
+CRM_HD double exp_fast_ok(double x, bool& ok) {
+  const double xc = fmin(fmax(x, -708.0), 709.0);
+  int m;
+  const dd y = exp_fast(xc, &m);  // y.hi in [0.99, 2), m in [-1022, 1023]
+  const double ax = fabs(x);
+  const bool one = ax <= 0x1p-54;  // e^x rounds to 1 (zeros included)
+  ok = one || ((x >= -708.0) && (x <= 709.0) && (ax >= 0x1p-26) && f64_decided(y, kRoundC64));
+  return one ? 1.0 : scale_exp(y.hi, m);
+}
+
 // Correctly rounded e^x, binary64.
 CRM_HD double cr_exp(double x) {
   if (x != x) return x + x;
@@ -278,28 +308,47 @@ CRM_HD double cr_exp(double x) {
   return exp_f64_slow(x);
 }
 
-// ---- f32 exp: one double with error < 2^-50, rounded once (R6) ---------------
-// e^x = 2^m * 2^(j/64) * e^r, k = rint(x 64/ln2) = 64 m + j, r = x - k ln2/64
-// (ln2/64 = C1 + C2, |r| <= ln2/128): e^r - 1 by a degree-6 Taylor polynomial
-// (truncation < 2^-66), 2^(j/64) correctly rounded: relative error < 2^-51.
-CRM_HD double exp_f64_of_f32(float xf) {
-  const float xc = fminf(fmaxf(xf, -104.0f), 89.0f);  // e^-104 < 2^-150 -> 0; e^89 -> inf
-  const double x = (double)xc;
+CRM_SLOW double cr_exp_slow(double x) { return cr_exp(x); }
+
+// ---- f32 exp: one double with error < 2^-49, rounded once (R6) ---------------
+// e^x = 2^m * 2^(j/128) * e^r with k = rint(x 128/ln2) = 128 m + j and r = x -
+// k ln2/128 (ln2/128 = C1 + C2 by two FMAs: |error| < 2^-60), |r| <= ln2/256 =
+// 2^-8.5: e^r - 1 by a degree-4 Taylor polynomial (truncation r^5/120 <
+// 2^-49.4 relative), 2^(j/128) correctly rounded: relative error < 2^-49,
+// i.e. < 16 ulps of the double — the f32 rounding test uses a 32-ulp margin
+// (kF32Margin), so an undecided element (probability ~2^-23) takes the
+// double-double accurate phase.  About 10 FP64 operations per element.
+// The evaluation for x in [-104, 89] (as a double; any other x gives a
+// meaningless but finite-or-NaN value: callers range-check).
+CRM_HD double exp_f64_of_f32_core(double x) {
   const double kShift = 0x1.8p52;  // 1.5 * 2^52: rint trick
-  const double ks = fma(x, 0x1.71547652b82fep+6, kShift);
+  const double ks = fma(x, 0x1.71547652b82fep+7, kShift);  // x 128/ln2 + shift
   const double k = ks - kShift;
   const int ki = (int)(bits_of(ks) & 0xffffffffu);
-  const double r = fma(-k, 0x1.62e42fefa39efp-7, x);
-  const double rr = fma(-k, 0x1.abc9e3b39803fp-62, r);
-  double p = fma(rr, 1.0 / 720.0, 1.0 / 120.0);
-  p = fma(p, rr, 1.0 / 24.0);
-  p = fma(p, rr, 1.0 / 6.0);
+  const double r = fma(-k, 0x1.62e42fefa39efp-8, x);    // C1 = RN(ln2/128)
+  const double rr = fma(-k, 0x1.abc9e3b39803fp-63, r);  // C2 = RN(ln2/128 - C1)
+  double p = fma(rr, 1.0 / 24.0, 1.0 / 6.0);
   p = fma(p, rr, 0.5);
   p = fma(p, rr, 1.0);
   p = p * rr;  // e^r - 1
-  const double t = CRM_TAB(kExp2Tab, ki & 63);
-  double y = fma(t, p, t);
-  y = double_of(bits_of(y) + ((uint64_t)(int64_t)(ki >> 6) << 52));
+  const double t = CRM_TAB(kExp2Tab, ki & 127);
+  const double y = fma(t, p, t);  // in [2^-1/256.., 2): scaling by 2^m touches the high word only
+  const uint64_t u = bits_of(y);
+  return double_of(((uint64_t)((uint32_t)(u >> 32) + ((uint32_t)(ki >> 7) << 20)) << 32) |
+                   (u & 0xffffffffu));
+}
+
+CRM_HD double exp_f64_of_f32_raw(float xf) {
+  const float xc = fminf(fmaxf(xf, -104.0f), 89.0f);  // e^-104 < 2^-150 -> 0; e^89 -> inf
+  return exp_f64_of_f32_core((double)xc);  // a NaN input is clamped: the caller handles NaN
+}
+
+// Inputs whose f32 e^x is a normal number (e^-87.33 > 2^-126, e^88.72 <
+// FLT_MAX): there the fast value's f32 rounding test on its low bits applies.
+CRM_HD bool expf_fast_range(float x) { return x >= -87.33f && x <= 88.72f; }
+
+CRM_HD double exp_f64_of_f32(float xf) {
+  const double y = exp_f64_of_f32_raw(xf);
   return (xf != xf) ? (double)xf : y;  // NaN passes through
 }
 
@@ -314,11 +363,12 @@ CRM_SLOW float exp_f32_slow(float x) {
   return f32_of_dd(fast_two_sum(y.hi * s, y.lo * s));
 }
 
-constexpr uint32_t kF32Margin = 32;  // double ulps (the fast value is within 2^-51: 4 ulps)
+constexpr uint32_t kF32Margin = 32;  // double ulps (the fast value is within 2^-49: 16 ulps)
 
 // Correctly rounded e^x, binary32.
 CRM_HD float cr_expf(float x) {
-  const double y = exp_f64_of_f32(x);
+  if (x != x) return x + x;
+  const double y = exp_f64_of_f32_raw(x);
   if (f32_decided(y, kF32Margin)) return (float)y;
   return exp_f32_slow(x);
 }
@@ -328,11 +378,14 @@ struct LogRed {
   double ed, r;  // log x = ed ln2 + T[j] + log1p(r), r exact
   int j;
 };
-// x finite, > 0
+// x finite, > 0 (kSub: subnormal x possible; without it x must be normal —
+// any other bit pattern gives a meaningless reduction with an in-range table
+// index, for callers that range-check)
+template <bool kSub = true>
 CRM_HD LogRed log_reduce(double x) {
   uint64_t u = bits_of(x);
   int e = (int)(u >> 52) - 1023;
-  if (e == -1023) {  // subnormal: scale into the normal range
+  if (kSub && e == -1023) {  // subnormal: scale into the normal range
     u = bits_of(x * 0x1p54);
     e = (int)(u >> 52) - 1023 - 54;
   }
@@ -355,11 +408,14 @@ CRM_HD dd log_fast(double x) {
   const LogRed red = log_reduce(x);
   const double r = red.r;
   const double Th = CRM_TAB(kLogT, 2 * red.j), Tl = CRM_TAB(kLogT, 2 * red.j + 1);
-  dd a = two_sum(red.ed * kLn2Hi, Th);  // ed * Ln2Hi exact (11 x 42 bits)
+  // ed * Ln2Hi is exact (11 x 42 bits) and, when not 0, larger than |Th| <=
+  // 0.41: Fast2Sum is exact
+  const dd a = fast_two_sum(red.ed * kLn2Hi, Th);
   const double alo = a.lo + fma(red.ed, kLn2Mid, Tl);
   const dd b = two_sum(a.hi, r);
   const dd sq = two_prod(r, r);
-  const dd c = two_sum(b.hi, -0.5 * sq.hi);
+  // |b.hi| >= 2^-8.1 or b.hi = r (e = 0, T = 0) dominates r^2/2: Fast2Sum
+  const dd c = fast_two_sum(b.hi, -0.5 * sq.hi);
   double Q = fma(r, 1.0 / 9, -1.0 / 8);
   Q = fma(Q, r, 1.0 / 7);
   Q = fma(Q, r, -1.0 / 6);
@@ -390,6 +446,15 @@ CRM_SLOW dd log_accurate(double x) {
 
 CRM_SLOW double log_f64_slow(double x) { return log_accurate(x).hi; }
 
+// Vectorisable fast phase of cr_log (see exp_fast_ok): x outside the normal
+// positive range (<= 0, subnormal, inf, NaN) is evaluated at 1 and flagged.
+CRM_HD double log_fast_ok(double x, bool& ok) {
+  const bool normal = (x >= 0x1p-1022) && (x < INFINITY);
+  const dd y = log_fast(normal ? x : 1.0);
+  ok = normal && f64_decided(y, kRoundC64);
+  return y.hi;
+}
+
 // Correctly rounded log x, binary64.
 CRM_HD double cr_log(double x) {
   if (!(x > 0) || x == INFINITY) {
@@ -401,17 +466,43 @@ CRM_HD double cr_log(double x) {
   return log_f64_slow(x);
 }
 
+CRM_SLOW double cr_log_slow(double x) { return cr_log(x); }
+
 CRM_SLOW float log_f32_slow(float x) { return f32_of_dd(log_accurate((double)x)); }
 
-// Correctly rounded log x, binary32: the double-double fast phase's high part
-// (within 2^-66: far inside the margin), rounded once.
+// f32 log as a double within 2^-51 (within a few double ulps): CUDA's log on
+// the device (<= 1 ulp), libm's on the host.  0 -> -inf, < 0 / NaN -> NaN,
+// inf -> inf, all exact.
+CRM_HD double log_f64_of_f32(float x) { return log((double)x); }
+
+// The hot-path f32 log for x a positive finite f32 (callers range-check):
+// log x = e ln2 + T[j] + log1p(r) with the exact reduction of log_reduce (an
+// f32 x is a normal double) and log1p(r) = r - r^2/2 + ... - r^8/8 by Horner
+// in double (|r| < 2^-7.48: truncation < 2^-67 absolute and < 2^-58 relative
+// to r), T[j] and e ln2 rounded: relative error < 2^-49 (16 ulps), the same
+// 32-ulp margin as f32 EXP.  ~12 FP64 operations.
+CRM_HD double logf_fast_core(float xf) {
+  const LogRed red = log_reduce<false>((double)xf);
+  const double r = red.r;
+  double q = fma(r, -1.0 / 8, 1.0 / 7);
+  q = fma(q, r, -1.0 / 6);
+  q = fma(q, r, 1.0 / 5);
+  q = fma(q, r, -0.25);
+  q = fma(q, r, 1.0 / 3);
+  q = fma(q, r, -0.5);
+  const double l1p = fma(r * r, q, r);  // log1p(r)
+  const double th = CRM_TAB(kLogT, 2 * red.j);
+  return fma(red.ed, kLn2Hi, th) + fma(red.ed, kLn2Mid, l1p);
+}
+// positive, finite, and not 1 (log 1 = +0 exactly; the sum above returns it
+// too, but 1 sits on the rounding test's edge): the fast phase applies
+CRM_HD bool logf_fast_range(float x) { return x > 0.0f && x < INFINITY; }
+
+// Correctly rounded log x, binary32: the double log (within 1 ulp) rounded
+// once when the rounding test decides it, else the double-double phase.
 CRM_HD float cr_logf(float x) {
-  if (!(x > 0) || x == INFINITY) {
-    if (x == 0) return -INFINITY;
-    return (x == INFINITY) ? x : (x - x) / (x - x);
-  }
-  const double y = log_fast((double)x).hi;
-  if (f32_decided(y, 2)) return (float)y;
+  const double y = log_f64_of_f32(x);
+  if (f32_decided(y, kF32Margin)) return (float)y;
   return log_f32_slow(x);
 }
 

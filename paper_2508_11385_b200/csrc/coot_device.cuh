@@ -660,7 +660,41 @@ __device__ __forceinline__ void bin_vec(T (&a)[W], const T (&b)[W]) {
   }
 }
 
+// The rare accurate phase of a W-element EXP / LOG: the undecided elements
+// go one by one through ONE call site (a local copy of the W inputs /
+// results; the hot path keeps its registers).
+// The rare accurate phase of a W-element EXP / LOG: every element of the
+// group is recomputed by the scalar correctly rounded function (the same
+// result for the ones the fast phase already decided) through ONE call site
+// with a local copy of the inputs / results, so the hot path keeps its
+// registers and stays straight-line.
 template <int OP, class T, int W>
+__device__ __noinline__ void slow_fix_call(const T (&x)[W], T (&v)[W]) {
+#pragma unroll 1
+  for (int w = 0; w < W; ++w) {
+    if constexpr (std::is_same<T, float>::value)
+      v[w] = (OP == COOT_OP_EXP) ? crm::cr_expf(x[w]) : crm::cr_logf(x[w]);
+    else
+      v[w] = (OP == COOT_OP_EXP) ? crm::cr_exp_slow(x[w]) : crm::cr_log_slow(x[w]);
+  }
+}
+template <int OP, class T, int W>
+__device__ __forceinline__ void slow_fix(const T (&x)[W], T (&v)[W]) {
+  T xs[W], vs[W];
+#pragma unroll
+  for (int w = 0; w < W; ++w) xs[w] = x[w];
+  slow_fix_call<OP, T, W>(xs, vs);
+#pragma unroll
+  for (int w = 0; w < W; ++w) v[w] = vs[w];
+}
+
+// EXP / LOG group size: the catalog kernels take 8 elements at a time (all
+// of a 2-unit dispatch: the most interleaving); the interpreter 4 (it holds
+// its register stack next to them).
+#ifndef COOT_EXP_GROUP
+#define COOT_EXP_GROUP 8
+#endif
+template <int OP, int GMAX = COOT_EXP_GROUP, class T, int W>
 __device__ __forceinline__ void un_vec(T (&v)[W]) {
   if constexpr (is_half<T>() && OP == COOT_OP_SQUARE) {
     half2_vec<COOT_OP_MUL, T, W>(v, v);
@@ -669,6 +703,43 @@ __device__ __forceinline__ void un_vec(T (&v)[W]) {
 #pragma unroll
     for (int w = 0; w < W; ++w) y[w] = un<OP>(to_f32(v[w]));
     half_round_vec<T, W>(y, v);
+  } else if constexpr ((std::is_same<T, float>::value || std::is_same<T, double>::value) &&
+                       (OP == COOT_OP_EXP || OP == COOT_OP_LOG)) {
+    // correctly rounded EXP / LOG (R6), in groups of up to 4 elements: the
+    // fast phase of the group first (straight-line, its chains interleave),
+    // then ONE rare branch if the rounding test left any element undecided.
+    // Groups of 4 bound the live registers (the interpreter evaluates 16
+    // elements per dispatch next to its register stack).
+    constexpr int G = W < GMAX ? W : GMAX;
+    static_assert(W % G == 0, "group size");
+#pragma unroll
+    for (int g = 0; g < W; g += G) {
+      T x[G];
+      bool all = true;
+#pragma unroll
+      for (int w = 0; w < G; ++w) {
+        x[w] = v[g + w];
+        if constexpr (std::is_same<T, float>::value) {
+          // outside the fast range (non-normal results, NaN, <= 0 for LOG)
+          // the fast value is meaningless and the slow path decides
+          const bool in = (OP == COOT_OP_EXP) ? crm::expf_fast_range(x[w]) : crm::logf_fast_range(x[w]);
+          const double y = (OP == COOT_OP_EXP) ? crm::exp_f64_of_f32_core((double)x[w])
+                                               : crm::logf_fast_core(x[w]);
+          all = all && in && crm::f32_mid_clear(y, crm::kF32Margin);
+          v[g + w] = (float)y;
+        } else {
+          bool ok;
+          v[g + w] = (OP == COOT_OP_EXP) ? crm::exp_fast_ok(x[w], ok) : crm::log_fast_ok(x[w], ok);
+          all = all && ok;
+        }
+      }
+      if (__builtin_expect(!all, 0)) {
+        T r[G];
+        slow_fix<OP, T, G>(x, r);
+#pragma unroll
+        for (int w = 0; w < G; ++w) v[g + w] = r[w];
+      }
+    }
   } else if constexpr (is_half<T>() && (OP == COOT_OP_EXP || OP == COOT_OP_LOG)) {
     float x[W], y[W];
     unsigned closest = 0xffffffffu;

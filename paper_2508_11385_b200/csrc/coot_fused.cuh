@@ -134,6 +134,7 @@ struct CatalogEval;
 template <int... Code>
 struct CatalogEval<StaticProg<Code...>> {
   static constexpr int K = StaticProg<Code...>::n_ops();
+  static constexpr int kStack = COOT_MAX_STACK;
   static constexpr bool kInterp = false;
   // the program is the plain matrix [L0]
   static constexpr bool kIdentity = sizeof...(Code) == 1 && StaticProg<Code...>::codes[0] == 0;
@@ -171,6 +172,7 @@ struct CatalogEval<StaticProg<Code...>> {
 template <int KMAX, int SMAX>
 struct InterpEval {
   static constexpr int K = KMAX;
+  static constexpr int kStack = SMAX;
   static constexpr bool kInterp = true;
   static constexpr bool kIdentity = false;
 
@@ -193,7 +195,7 @@ struct InterpEval {
 #define COOT_UN_CASE(OP, d)                                                \
   case COOT_KEY(COOT_OP_##OP, d):                                          \
     if constexpr ((d) >= 1 && (d) <= SMAX && op_legal<T>(COOT_OP_##OP)) {  \
-      un_vec<COOT_OP_##OP>(st[(d) >= 1 ? (d) - 1 : 0]);                    \
+      un_vec<COOT_OP_##OP, 4>(st[(d) >= 1 ? (d) - 1 : 0]);                 \
     } else if constexpr ((d) >= 1 && (d) <= SMAX) {                        \
       __trap(); /* op illegal for T: rejected on the host (R9) */          \
     }                                                                      \
@@ -468,14 +470,19 @@ constexpr int units_per_dispatch() {
 #define COOT_INTERP4_MINB 2
 #endif
 #ifndef COOT_INTERP4_UD
-#define COOT_INTERP4_UD 4
+#define COOT_INTERP4_UD 2
+#endif
+#ifndef COOT_INTERP2_UD
+#define COOT_INTERP2_UD 4
 #endif
 // fused_tma_kernel: the small interpreter on 4-byte types takes 4 units (16
 // elements) per dispatch — halving the per-element cost of its uniform
 // instruction dispatch; the host sizes those tiles at 4 * 256 units.
 template <class T, class EV>
 constexpr int tma_units_per_dispatch() {
-  return (EV::kInterp && EV::K <= 4 && sizeof(T) == 4) ? COOT_INTERP4_UD : units_per_dispatch<T, EV>();
+  return (EV::kInterp && EV::K <= 4 && sizeof(T) == 4)
+             ? (EV::kStack <= 2 ? COOT_INTERP2_UD : COOT_INTERP4_UD)
+             : units_per_dispatch<T, EV>();
 }
 // Resident CTAs per SM the register budget is sized for: 2 (<= 96 registers),
 // except the 8-operand interpreter, which gets the whole register file.
@@ -484,9 +491,28 @@ constexpr int tma_min_ctas() {
   return (EV::kInterp && EV::K > 4) ? 1 : (EV::kInterp ? COOT_INTERP4_MINB : 2);
 }
 
+// In-band producer for the small interpreter: the CTA is the 8 consumer warps
+// only (256 threads) and consumer thread 0 issues the bulk copies — the first
+// S tiles up front, then the refill of each stage as soon as all 8 warps have
+// released it.  Two 256-thread CTAs per SM get 128 registers per thread (a
+// 288-thread CTA is allocated registers for 10 warps: 96), which is what the
+// interpreter's register stack of 4 units x 4 slots needs without spilling.
+#ifndef COOT_INTERP_INBAND
+#define COOT_INTERP_INBAND 1
+#endif
+template <class EV>
+constexpr bool tma_inband() {
+  return COOT_INTERP_INBAND && EV::kInterp && EV::K <= 4;
+}
+template <class EV>
+constexpr int tma_threads() {
+  return tma_inband<EV>() ? kConsumerWarps * 32 : kTmaThreads;
+}
+
 template <class T, int ACC, class EV>
-__global__ void __launch_bounds__(kTmaThreads, tma_min_ctas<EV>())
+__global__ void __launch_bounds__(tma_threads<EV>(), tma_min_ctas<EV>())
     fused_tma_kernel(const __grid_constant__ FusedArgs a) {
+  constexpr bool kInband = tma_inband<EV>();
   pdl_wait();
   constexpr int W = Unit<T>::W;
   constexpr int K = EV::K;
@@ -510,8 +536,24 @@ __global__ void __launch_bounds__(kTmaThreads, tma_min_ctas<EV>())
   acc.init();
   const u64 ntiles = (a.nunits + TU - 1) / TU;
   const u64 boff = a.head * sizeof(T);  // body starts 16-byte aligned here
+  // the bulk copies of this CTA's j-th tile into stage j % S
+  auto issue = [&](u64 t, uint32_t st, uint64_t pol) {
+    const u64 u0 = t * TU;
+    const uint32_t nu = (uint32_t)((a.nunits - u0) < TU ? (a.nunits - u0) : TU);
+    mbar_expect_tx(&full[st], nu * 16u * nk);
+    for (uint32_t k = 0; k < nk; ++k)
+      bulk_g2s(smem + ((size_t)st * nk + k) * tile_bytes,
+               reinterpret_cast<const char*>(a.in[k]) + boff + u0 * 16, nu * 16u, &full[st], pol);
+  };
+  if constexpr (kInband) {
+    if (threadIdx.x == 0) {
+      const uint64_t pol = policy_evict_first();
+      u64 t = blockIdx.x;
+      for (uint32_t st = 0; st < S && t < ntiles; ++st, t += gridDim.x) issue(t, st, pol);
+    }
+  }
 
-  if (warp == kConsumerWarps) {
+  if (!kInband && warp == kConsumerWarps) {
     // ---------------- producer ----------------
     if (lane == 0) {
       const uint64_t pol = policy_evict_first();
@@ -576,6 +618,15 @@ __global__ void __launch_bounds__(kTmaThreads, tma_min_ctas<EV>())
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
+      if constexpr (kInband) {
+        // refill this stage with the tile S rounds ahead once every warp has
+        // released it (thread 0 waits for the slowest warp of the CTA)
+        const u64 tn = t + (u64)S * gridDim.x;
+        if (threadIdx.x == 0 && tn < ntiles) {
+          producer_wait(&empty[s], ph, a.producer_sleep);
+          issue(tn, s, policy_evict_first());
+        }
+      }
       if (++s == S) {
         s = 0;
         ph ^= 1u;

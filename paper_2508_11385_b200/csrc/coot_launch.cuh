@@ -67,7 +67,10 @@ FusedFn pick_fused_acc(int catalog, int interp_large, int driver) {
           break;
       }
     }
-    if (interp_large) return driver_kernel<T, ACC, InterpEval<8, 8>, 1>(driver);
+    if (interp_large == 1) return driver_kernel<T, ACC, InterpEval<8, 8>, 1>(driver);
+    // shallow programs (fused stack depth <= 2) on the TMA driver: a 2-slot
+    // stack leaves the registers for 4 units (16 elements) per dispatch
+    if (interp_large == 2 && driver == 1) return &fused_tma_kernel<T, ACC, InterpEval<4, 2>>;
     return driver_kernel<T, ACC, InterpEval<4, 4>, 1>(driver);
   }
 }
@@ -130,7 +133,10 @@ cudaError_t launch_fused_t(const FusedPlan& p, const FusedArgs& a, cudaStream_t 
   if (p.driver == 1 || p.driver == 3) {
     cudaError_t e = allow_smem(reinterpret_cast<const void*>(k), p.smem);
     if (e != cudaSuccess) return e;
-    return launch_k(k, p.grid, kTmaThreads, p.smem, s, a, p.pdl);
+    // fused_tma_kernel with the small interpreter: in-band producer, 8 warps
+    const bool inband = COOT_INTERP_INBAND && p.driver == 1 && p.catalog < 0 && p.interp_large != 1;
+    return launch_k(k, p.grid, inband ? (unsigned)kConsumerWarps * 32 : (unsigned)kTmaThreads,
+                    p.smem, s, a, p.pdl);
   }
   return launch_k(k, p.grid, kThreads, 0, s, a, p.pdl);
 }
@@ -139,7 +145,7 @@ cudaError_t launch_fused_t(const FusedPlan& p, const FusedArgs& a, cudaStream_t 
 template <class T, template <class, class> class KER>
 DimFn pick_dim_ev(const DimPlan& p) {
   if (p.catalog == 0) return KER<T, CatalogEval<StaticProg<CL(0)>>>::run;
-  if (p.interp_large) return KER<T, InterpEval<8, 8>>::run;
+  if (p.interp_large == 1) return KER<T, InterpEval<8, 8>>::run;
   return KER<T, InterpEval<4, 4>>::run;
 }
 

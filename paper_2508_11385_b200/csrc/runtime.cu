@@ -410,8 +410,9 @@ int match_catalog(const coot_expr* e) {
   return -1;
 }
 
-// Pack everything the evaluators need into the kernel arguments.
-void fill_program(const coot_expr* e, coot::FusedArgs* a) {
+// Pack everything the evaluators need into the kernel arguments.  Returns the
+// deepest stack the dispatched (fused-operand) program reaches.
+int fill_program(const coot_expr* e, coot::FusedArgs* a) {
   for (uint32_t k = 0; k < COOT_MAX_OPERANDS; ++k)
     a->in[k] = k < e->n_operands ? e->operands[k].ptr : nullptr;
   for (uint32_t s = 0; s < COOT_MAX_SCALARS; ++s)
@@ -428,7 +429,7 @@ void fill_program(const coot_expr* e, coot::FusedArgs* a) {
   // ADD / SUB / MUL that consumes it becomes one dispatch (the device has fused
   // cases for those three only: more cases cost the small interpreter spills).  The stack is never
   // deeper than in the original program.
-  int sp = 0;
+  int sp = 0, max_sp = 0;
   uint32_t n = 0;
   const uint32_t ni = e->n_instr;
   auto emit = [&](int key, int arg) { a->code[n++] = (uint32_t)key | ((uint32_t)arg << 16); };
@@ -451,13 +452,16 @@ void fill_program(const coot_expr* e, coot::FusedArgs* a) {
       emit(COOT_KEY(COOT_XOP_S(nx2), sp + 1), arg);
       i += 2;
       ++sp;
+      max_sp = std::max(max_sp, sp);
       continue;
     }
     emit(COOT_KEY(op, sp), arg);
     if (op == COOT_OP_LOAD || op == COOT_OP_SCALAR) ++sp;
     else if (is_binary(op)) --sp;
+    max_sp = std::max(max_sp, sp);
   }
   a->n_instr = n;
+  return max_sp;
 }
 
 int acc_for_kind(uint32_t kind) {
@@ -667,7 +671,7 @@ coot_status run_fused(coot_ctx* ctx, const coot_expr* e, const Shape& sh, int ac
   const u64 W = 16 / es;
   coot::FusedArgs a;
   memset(&a, 0, sizeof a);
-  fill_program(e, &a);
+  const int fused_depth = fill_program(e, &a);
   a.out = out;
   a.n = n;
   // 16-byte unit path iff every accessed array has the same misalignment.
@@ -697,6 +701,12 @@ coot_status run_fused(coot_ctx* ctx, const coot_expr* e, const Shape& sh, int ac
   p.catalog = (ctx->flags & COOT_INIT_FORCE_INTERP) ? -1 : match_catalog(e);
   if (acc >= coot::ACC_VAR && p.catalog > 0) p.catalog = -1;  // see pick_fused_acc
   p.interp_large = (e->n_operands > 4 || sh.max_depth > 4) ? 1 : 0;
+  // shallow interpreter class (TMA driver, 4-byte types): a 2-slot stack, 4
+  // units per dispatch (coot_launch.cuh pick_fused_acc)
+  static const bool no_shallow = env_int("COOT_NO_SHALLOW_INTERP", 0) != 0;  // A/B aid
+  if (p.catalog < 0 && !p.interp_large && p.driver == 1 && elem_size(e->elem) == 4 &&
+      fused_depth <= 2 && !no_shallow)
+    p.interp_large = 2;
   u64 grid;
   if (p.driver == 1) {
     // TMA driver geometry: a function of (n, operands, SM count, evaluator
@@ -707,7 +717,7 @@ coot_status run_fused(coot_ctx* ctx, const coot_expr* e, const Shape& sh, int ac
     // on 4-byte types evaluates 4 units per dispatch, so its tiles hold >= 4 *
     // 256 units (coot::tma_units_per_dispatch).
     const u64 nk = e->n_operands;  // compacted: every operand is referenced
-    const bool wide_dispatch = p.catalog < 0 && !p.interp_large && elem_size(e->elem) == 4;
+    const bool wide_dispatch = p.catalog < 0 && p.interp_large != 1 && elem_size(e->elem) == 4;
     u64 tu = (nk <= 3 || wide_dispatch) ? 2 * coot::kTileUnits : coot::kTileUnits;
     if (ctx->tma_tile_units)  // override, still >= what the evaluator's dispatch needs
       tu = std::max<u64>((u64)ctx->tma_tile_units,
@@ -746,7 +756,7 @@ coot_status run_fused(coot_ctx* ctx, const coot_expr* e, const Shape& sh, int ac
   p.grid = (unsigned)grid;
   if (ctx->log)
     fprintf(stderr, "[coot] fused elem=%u n=%llu path=%d%s acc=%d driver=%d grid=%u smem=%u stages=%u tile=%u head=%llu units=%llu\n",
-            e->elem, (unsigned long long)n, p.catalog, p.catalog < 0 ? (p.interp_large ? "(interp8)" : "(interp4)") : "",
+            e->elem, (unsigned long long)n, p.catalog, p.catalog < 0 ? (p.interp_large == 1 ? "(interp8)" : p.interp_large == 2 ? "(interp2)" : "(interp4)") : "",
             acc, p.driver, p.grid, p.smem, a.stages, a.tile_units, (unsigned long long)a.head,
             (unsigned long long)a.nunits);
   cudaError_t ce = dispatch_fused(e->elem, p, a, ctx->stream);

@@ -24,3 +24,27 @@ void crm_log_phases(const double* x, double* rel, int* decided, long n) {
   }
 }
 }
+extern "C" {
+void crm_exp_batched(const double* x, double* y, long n) {
+  for (long i = 0; i < n; ++i) { bool ok; double v = exp_fast_ok(x[i], ok); y[i] = ok ? v : cr_exp_slow(x[i]); }
+}
+void crm_log_batched(const double* x, double* y, long n) {
+  for (long i = 0; i < n; ++i) { bool ok; double v = log_fast_ok(x[i], ok); y[i] = ok ? v : cr_log_slow(x[i]); }
+}
+}
+extern "C" {
+// the device's vectorised f32 path (coot_device.cuh un_vec): fast value when
+// in range and clear of a midpoint, else the scalar correctly rounded function
+void crm_expf_vec(const float* x, float* y, long n) {
+  for (long i = 0; i < n; ++i) {
+    const double v = exp_f64_of_f32_core((double)x[i]);
+    y[i] = (expf_fast_range(x[i]) && f32_mid_clear(v, kF32Margin)) ? (float)v : cr_expf(x[i]);
+  }
+}
+void crm_logf_vec(const float* x, float* y, long n) {
+  for (long i = 0; i < n; ++i) {
+    const double v = logf_fast_core(x[i]);
+    y[i] = (logf_fast_range(x[i]) && f32_mid_clear(v, kF32Margin)) ? (float)v : cr_logf(x[i]);
+  }
+}
+}
