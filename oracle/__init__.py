@@ -92,6 +92,14 @@ def lib():
         L.orc_stats.argtypes = [i32, i32, u64, vp, vp]
         L.orc_sum_dim.restype = i32
         L.orc_sum_dim.argtypes = [i32, i32, u64, u64, vp, vp]
+        L.orc_rows_new.restype = vp
+        L.orc_rows_new.argtypes = [i32, u64]
+        L.orc_rows_free.restype = None
+        L.orc_rows_free.argtypes = [vp]
+        L.orc_rows_add.restype = i32
+        L.orc_rows_add.argtypes = [vp, u64, u64, u64, u64, vp]
+        L.orc_rows_final.restype = i32
+        L.orc_rows_final.argtypes = [vp, vp]
         L.orc_run_chunked.restype = i32
         L.orc_run_chunked.argtypes = [i32, u64, u64, u64, i32, ctypes.POINTER(i32), u64, u64,
                                       vp, i32, ctypes.POINTER(i32), ctypes.POINTER(i32), i32,
@@ -261,3 +269,71 @@ def run_chunked(etype: str, program, fills, *, start: int, count: int, n_rows: i
                                  acc._buf if acc else None,
                                  _ptr(out) if out is not None else None), "run_chunked")
     return (acc.final() if acc else None), out
+
+
+class RowSums:
+    """sum(X, 1) fed a block of columns at a time (orc_rows_*): the per-row
+    state of orc_sum_dim's dim-1 loop kept between calls.  add(X, i0) takes a
+    column-major block (rows x ncols, element (i, j) at X[i + j*rows]) of rows
+    i0..; blocks must arrive in column order for each row.  Bit-identical to a
+    one-shot sum_dim(..., 1, ...) (tested); calls on disjoint row ranges may run
+    on different threads."""
+
+    def __init__(self, etype: str, n_rows: int):
+        self.etype, self.m = etype, n_rows
+        self._h = lib().orc_rows_new(TYPES[etype], n_rows)
+        if not self._h:
+            raise OracleError("orc_rows_new failed")
+
+    def add(self, X: np.ndarray, i0: int = 0, rows: int | None = None, ld: int | None = None):
+        X = np.ascontiguousarray(X, dtype=DTYPES[self.etype]).reshape(-1)
+        ld = ld if ld is not None else (rows if rows is not None else self.m)
+        rows = rows if rows is not None else ld
+        ncols = X.size // ld if ld else 0
+        _check(lib().orc_rows_add(self._h, i0, rows, ncols, ld, _ptr(X)), "rows_add")
+
+    def add_rows_of(self, X: np.ndarray, ld: int, i0: int, rows: int):
+        """Add rows i0..i0+rows-1 of a column-major block with leading dimension ld."""
+        X = np.ascontiguousarray(X, dtype=DTYPES[self.etype]).reshape(-1)
+        ncols = X.size // ld
+        base = X[i0:]  # element (i0 + i, j) at base[i + j*ld]
+        _check(lib().orc_rows_add(self._h, i0, rows, ncols, ld, _ptr(base)), "rows_add")
+
+    def final(self) -> np.ndarray:
+        out = np.empty(self.m, dtype=RDTYPES[self.etype])
+        _check(lib().orc_rows_final(self._h, _ptr(out)), "rows_final")
+        return out
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib().orc_rows_free(self._h)
+            self._h = None
+
+
+def stream_chunks(etype: str, program, fills, *, start: int, count: int, n_rows: int = 1,
+                  seed: int = 42, modk: int = 1, scalars=(), chunk: int = 1 << 24,
+                  threads: int | None = None):
+    """Yield (offset, z) for consecutive chunks of [start, start+count) IN INDEX
+    ORDER, z = the program's element-wise result over that chunk (each chunk is
+    orc_run_chunked's own regenerate + eval, so bit-identical to one run).  The
+    chunks are computed ahead on `threads` worker threads (ctypes releases the
+    GIL); the caller consumes them in order, e.g. feeding an Accumulator, so a
+    reduction sees exactly the sequential index order."""
+    import concurrent.futures as cf
+    threads = threads or max(1, min(32, os.cpu_count() or 1))
+    offs = list(range(0, count, chunk))
+
+    def one(off):
+        _, z = run_chunked(etype, program, fills, start=start + off,
+                           count=min(chunk, count - off), n_rows=n_rows, seed=seed, modk=modk,
+                           scalars=scalars, want_out=True, chunk=chunk)
+        return z
+
+    with cf.ThreadPoolExecutor(threads) as ex:
+        pending = {}
+        nxt = 0
+        for k, off in enumerate(offs):
+            while nxt < len(offs) and nxt < k + 2 * threads:
+                pending[nxt] = ex.submit(one, offs[nxt])
+                nxt += 1
+            yield off, pending.pop(k).result()

@@ -53,7 +53,7 @@ enum { ORC_ACCU = 0, ORC_RMIN = 1, ORC_RMAX = 2, ORC_MINMAX = 3, ORC_NORM2 = 4 }
 
 enum {
   ORC_E_OK = 0, ORC_E_TYPE = -1, ORC_E_PROGRAM = -2, ORC_E_NOMEM = -3,
-  ORC_E_EMPTY = -4, ORC_E_KIND = -5
+  ORC_E_EMPTY = -4, ORC_E_KIND = -5, ORC_E_SHAPE = -6
 };
 
 static size_t esize(int type) {
@@ -793,6 +793,13 @@ int orc_stats(int type, int kind, uint64_t n, const void* v, void* result) {
   return ORC_E_OK;
 }
 
+typedef struct orc_rows_s orc_rows;
+orc_rows* orc_rows_new(int type, uint64_t m);
+void orc_rows_free(orc_rows* r);
+int orc_rows_add(orc_rows* r, uint64_t i0, uint64_t rows, uint64_t ncols, uint64_t ld,
+                 const void* X);
+int orc_rows_final(const orc_rows* r, void* out);
+
 /* ---- dimension sums (reading R3) ----------------------------------------
  * X is column-major m x n (element (i,j) at X[i + j*m]).
  * dim 0: out[j] = sum_{i=0..m-1} X(i,j)   (n_cols results, a Row)
@@ -804,7 +811,6 @@ int orc_stats(int type, int kind, uint64_t n, const void* v, void* result) {
 int orc_sum_dim(int type, int dim, uint64_t m, uint64_t n, const void* X, void* out) {
   size_t es = esize(type);
   if (es == 0) return ORC_E_TYPE;
-  int is_float = is_flt(type);
   if (dim == 0) {
     for (uint64_t j = 0; j < n; ++j) {
       orc_acc a;
@@ -815,37 +821,83 @@ int orc_sum_dim(int type, int dim, uint64_t m, uint64_t n, const void* X, void* 
     return ORC_E_OK;
   }
   if (dim != 1) return ORC_E_KIND;
-  long double* s = NULL;
-  long double* c = NULL;
-  uint64_t* u = NULL;
+  orc_rows* r = orc_rows_new(type, m);
+  if (!r) return ORC_E_NOMEM;
+  orc_rows_add(r, 0, m, n, m, X);
+  orc_rows_final(r, out);
+  orc_rows_free(r);
+  return ORC_E_OK;
+}
+
+/* ---- dim-1 sums fed column block by column block -------------------------
+ * The per-row state of orc_sum_dim's dim-1 loop (Neumaier s, c per row for
+ * floats, a modular u64 per row for integers), kept between calls so a
+ * matrix too large for host RAM can be fed a block of columns at a time, in
+ * column order: orc_rows_add(r, i0, rows, ncols, ld, X) adds columns
+ * X(:, 0..ncols-1) of rows i0..i0+rows-1 (element (i, j) at X[i + j*ld]) to
+ * rows i0.. of the state.  Each row still sums j = 0..n-1 in order, so any
+ * split into column blocks, and any split of the rows between callers, gives
+ * exactly orc_sum_dim's arithmetic (tested). */
+struct orc_rows_s {
+  int type;
+  uint64_t m;
+  long double* s;
+  long double* c;
+  uint64_t* u;
+};
+
+orc_rows* orc_rows_new(int type, uint64_t m) {
+  if (esize(type) == 0) return NULL;
+  orc_rows* r = (orc_rows*)calloc(1, sizeof(orc_rows));
+  if (!r) return NULL;
   size_t mm = m ? m : 1;
-  if (is_float) {
-    s = (long double*)calloc(mm, sizeof(long double));
-    c = (long double*)calloc(mm, sizeof(long double));
-    if (!s || !c) { free(s); free(c); return ORC_E_NOMEM; }
+  r->type = type;
+  r->m = m;
+  if (is_flt(type)) {
+    r->s = (long double*)calloc(mm, sizeof(long double));
+    r->c = (long double*)calloc(mm, sizeof(long double));
   } else {
-    u = (uint64_t*)calloc(mm, sizeof(uint64_t));
-    if (!u) return ORC_E_NOMEM;
+    r->u = (uint64_t*)calloc(mm, sizeof(uint64_t));
   }
-  for (uint64_t j = 0; j < n; ++j) {
-    const char* col = (const char*)X + (size_t)(j * m) * es;
-    for (uint64_t i = 0; i < m; ++i) {
-      if (is_float) neumaier(&s[i], &c[i], elem_as_ld(type, col, i));
-      else u[i] += elem_as_u64(type, col, i);
+  if (is_flt(type) ? (!r->s || !r->c) : !r->u) {
+    orc_rows_free(r);
+    return NULL;
+  }
+  return r;
+}
+
+void orc_rows_free(orc_rows* r) {
+  if (!r) return;
+  free(r->s);
+  free(r->c);
+  free(r->u);
+  free(r);
+}
+
+int orc_rows_add(orc_rows* r, uint64_t i0, uint64_t rows, uint64_t ncols, uint64_t ld,
+                 const void* X) {
+  if (i0 + rows > r->m || (ncols > 0 && rows > ld)) return ORC_E_SHAPE;
+  size_t es = esize(r->type);
+  for (uint64_t j = 0; j < ncols; ++j) {
+    const char* col = (const char*)X + (size_t)(j * ld) * es;
+    for (uint64_t i = 0; i < rows; ++i) {
+      if (r->s) neumaier(&r->s[i0 + i], &r->c[i0 + i], elem_as_ld(r->type, col, i));
+      else r->u[i0 + i] += elem_as_u64(r->type, col, i);
     }
   }
-  for (uint64_t i = 0; i < m; ++i) {
-    switch (type) {
-      case ORC_F32: ((float*)out)[i] = (float)((__float128)s[i] + (__float128)c[i]); break;
-      case ORC_F64: ((double*)out)[i] = (double)((__float128)s[i] + (__float128)c[i]); break;
-      case ORC_U32: ((uint32_t*)out)[i] = (uint32_t)u[i]; break;
-      case ORC_S64: ((uint64_t*)out)[i] = u[i]; break;
-      default: store_flt(type, out, i, (__float128)s[i] + (__float128)c[i]); break;
+  return ORC_E_OK;
+}
+
+/* out: m results (eT; f32 for the fp8 storage types), each row's exact-ish
+ * Neumaier state rounded once. */
+int orc_rows_final(const orc_rows* r, void* out) {
+  for (uint64_t i = 0; i < r->m; ++i) {
+    switch (r->type) {
+      case ORC_U32: ((uint32_t*)out)[i] = (uint32_t)r->u[i]; break;
+      case ORC_S64: ((uint64_t*)out)[i] = r->u[i]; break;
+      default: store_flt(r->type, out, i, (__float128)r->s[i] + (__float128)r->c[i]); break;
     }
   }
-  free(s);
-  free(c);
-  free(u);
   return ORC_E_OK;
 }
 

@@ -62,8 +62,17 @@ def test_c2_full(ctx, store):
     assert abs(r[0].item() / (m * n) - 2.8179021514544039) < 1e-3
 
 
+def _pool():
+    import concurrent.futures as cf
+    import os
+    return cf.ThreadPoolExecutor(max(1, min(32, os.cpu_count() or 1)))
+
+
 def test_c3_sum_dims_full(ctx):
-    """configs[2]: sum(X,0), sum(X,1) on a 32768 x 32768 f64 column-major Mat."""
+    """configs[2]: sum(X,0), sum(X,1) on a 32768 x 32768 f64 column-major Mat:
+    ALL 32768 column sums and ALL 32768 row sums against the oracle, which
+    regenerates the matrix a block of columns at a time (column sums per block,
+    row sums through the resumable dim-1 state, rows split over threads)."""
     m = n = 32768
     X = dev_fill(ctx, "f64", m * n, 0, n_rows=m)
     d0 = torch.empty(n, dtype=torch.float64, device="cuda")
@@ -73,23 +82,26 @@ def test_c3_sum_dims_full(ctx):
     ctx.reduce("f64", m, n, [("LOAD", 0)], [X], [], "SUM_DIM1", d1)
     ctx.reduce("f64", m, n, [("LOAD", 0)], [X], [], "ACCU", tot)
     torch.cuda.synchronize()
+    del X
     d0h, d1h = d0.cpu().numpy(), d1.cpu().numpy()
-    rng = np.random.default_rng(0)
-    # sampled columns: the oracle sums each column from its own regenerated data
-    for j in list(rng.integers(0, n, 12)) + [0, n - 1]:
-        col = oracle.fill("f64", "randu", m, stream=0, start=int(j) * m)
-        assert_reduction(d0h[j], oracle.reduce("f64", "ACCU", col), "f64", "ACCU")
-    # sampled rows: regenerate the matrix chunk by chunk, feed each sampled row in
-    # column order to an oracle accumulator (exactly the oracle's dim-1 order)
-    rows = sorted(set([0, m - 1] + list(rng.integers(0, m, 6))))
-    accs = {i: oracle.Accumulator("f64", "ACCU") for i in rows}
-    step = 2048
-    for c0 in range(0, n, step):
-        chunk = oracle.fill("f64", "randu", m * step, stream=0, start=c0 * m).reshape(step, m)
-        for i in rows:
-            accs[i].add(chunk[:, i])
-    for i in rows:
-        assert_reduction(d1h[i], accs[i].final(), "f64", "ACCU")
+    want0 = np.empty(n)
+    rows = oracle.RowSums("f64", m)
+    bc, nt = 1024, 16
+    rs = m // nt
+    with _pool() as ex:
+        for c0 in range(0, n, bc):
+            parts = list(ex.map(lambda k: oracle.fill("f64", "randu", m * (bc // nt), stream=0,
+                                                       start=(c0 + k * (bc // nt)) * m),
+                                range(nt)))
+            blk = np.concatenate(parts)
+            sums = list(ex.map(lambda k: oracle.sum_dim("f64", 0, parts[k], m, bc // nt),
+                               range(nt)))
+            want0[c0:c0 + bc] = np.concatenate(sums)
+            list(ex.map(lambda k: rows.add_rows_of(blk, m, k * rs, rs), range(nt)))
+    want1 = rows.final()
+    for got, want in ((d0h, want0), (d1h, want1)):
+        rel = np.abs(got - want) / np.abs(want)
+        assert rel.max() <= 1e-12, (int(np.argmax(rel)), rel.max())
     # invariant: accu(sum(X,0)) == accu(sum(X,1)) == accu(X) within 1e-12
     t = float(tot[0].item())
     assert abs(d0h.sum() - t) <= 1e-12 * t and abs(d1h.sum() - t) <= 1e-12 * t
@@ -101,22 +113,24 @@ _C4_ORACLE = {}
 @pytest.mark.parametrize("etype", ["u32", "s64"])
 @pytest.mark.parametrize("store", [False, True])
 def test_c4_full_bit_exact(ctx, etype, store):
-    """configs[3]: X % Y + 7*Z with min/max reduction, 2^28 elements, bit-exact."""
+    """configs[3]: X % Y + 7*Z with min/max reduction, 2^28 elements, bit-exact;
+    stored form: ALL 2^28 elements against the oracle."""
     n = 1 << 28
     ops = [dev_fill(ctx, etype, n, s) for s in range(3)]
     out = torch.empty(n, dtype=TORCH[etype], device="cuda") if store else None
     r = torch.zeros(2, dtype=TORCH[etype], device="cuda")
     ctx.reduce(etype, n, 1, C4, ops, [7], "MINMAX", r, out)
     torch.cuda.synchronize()
-    if etype not in _C4_ORACLE:
-        _C4_ORACLE[etype], _ = oracle.run_chunked(etype, C4, ["randu"] * 3, start=0, count=n,
-                                                  scalars=[7], kind="MINMAX")
+    del ops
+    if etype not in _C4_ORACLE or store:
+        acc = oracle.Accumulator(etype, "MINMAX")
+        for off, z in oracle.stream_chunks(etype, C4, ["randu"] * 3, start=0, count=n,
+                                           scalars=[7]):
+            acc.add(z)
+            if store:
+                assert np.array_equal(to_host(out[off:off + z.size], etype), z), off
+        _C4_ORACLE[etype] = acc.final()
     assert np.array_equal(to_host(r, etype), _C4_ORACLE[etype])
-    if store:  # element-wise on the first, a middle and the last 2^22 elements
-        for s0 in (0, n // 2 + 12345, n - (1 << 22)):
-            _, z = oracle.run_chunked(etype, C4, ["randu"] * 3, start=s0, count=1 << 22,
-                                      scalars=[7], want_out=True)
-            assert np.array_equal(to_host(out[s0:s0 + (1 << 22)], etype), z)
 
 
 def _shard_consistency(coot, ctx, etype, prog, ops, sc, kind, n, nparts=16):
@@ -130,12 +144,24 @@ def _shard_consistency(coot, ctx, etype, prog, ops, sc, kind, n, nparts=16):
     return res
 
 
+def _oracle_full(etype, prog, k, n, sc, kind, out=None, ulp=0):
+    """The oracle over all n elements (threaded chunks, index-order reduction);
+    if `out` (device) is given, every element is compared with it on the way."""
+    acc = oracle.Accumulator(etype, kind)
+    for off, z in oracle.stream_chunks(etype, prog, ["randu"] * k, start=0, count=n,
+                                       scalars=sc):
+        acc.add(z)
+        if out is not None:
+            assert_elementwise(to_host(out[off:off + z.size], etype), z, etype, max_ulp=ulp)
+    return acc.final()
+
+
 @pytest.mark.parametrize("kind", ["dot", "norm2"])
 def test_c5_full_2p32(coot, ctx, kind):
-    """configs[4]: dot(x, y) and norm2(x) on 2^32-element f32 Cols (one GPU holds
-    the whole vector here; the row-block sharding is exercised by the shard
-    checks).  Closed form on ones; randu: one 2^28 shard vs the oracle, and the
-    full launch vs the rank-order combine of 16 shard partials."""
+    """configs[4]: dot(x, y) and norm2(x) on 2^32-element f32 Cols of randu data
+    against the oracle over all 2^32 elements; closed form on ones; and the
+    full launch vs the rank-order combine of 16 row-block shard partials (the
+    sharded N>1 path)."""
     n = 1 << 32
     prog = [("LOAD", 0), ("LOAD", 1), ("MUL", 0)] if kind == "dot" else [("LOAD", 0)]
     red = "ACCU" if kind == "dot" else "NORM2"
@@ -152,33 +178,33 @@ def test_c5_full_2p32(coot, ctx, kind):
     res = _shard_consistency(coot, ctx, "f32", prog, ops, [], red, n)
     torch.cuda.synchronize()
     assert abs(res[0].item() - full) <= 1e-5 * abs(full)
-    # one 2^28 shard against the oracle (its own launch on the shard view)
-    s0, cnt = 3 << 28, 1 << 28
-    ctx.reduce("f32", cnt, 1, prog, [o[s0:s0 + cnt] for o in ops], [], red, r)
-    torch.cuda.synchronize()
-    want, _ = oracle.run_chunked("f32", prog, ["randu"] * k, start=s0, count=cnt, kind=red)
-    assert_reduction(r[0].item(), want, "f32", red)
+    del ops
+    assert_reduction(full, _oracle_full("f32", prog, k, n, [], red), "f32", red)
     # statistical wiring: E[xy] = 1/4, E[x^2] = 1/3
     expect = n / 4 if kind == "dot" else (n / 3) ** 0.5
     assert abs(full / expect - 1) < 1e-3
 
 
-@pytest.mark.parametrize("form", ["c2_reduce", "axpy"])
+@pytest.mark.parametrize("form", ["c2_reduce", "c2_stored", "axpy_in_place"])
 def test_headline_2p30(coot, ctx, form):
-    """north-star target size: f32 expression + accu on 2^30 elements."""
+    """north-star target size, the three forms bench.py times: f32 expression +
+    accu on 2^30 elements; accu against the oracle over all 2^30 elements and,
+    for the stored forms, every element bit-exact."""
     n = 1 << 30
-    prog, sc, k = (C2, [3.0], 3) if form == "c2_reduce" else (C1_AXPY, [2.5], 2)
+    c2 = form.startswith("c2")
+    prog, sc, k = (C2, [3.0], 3) if c2 else (C1_AXPY, [2.5], 2)
     ops = [dev_fill(ctx, "f32", n, s) for s in range(k)]
     r = torch.zeros(2, device="cuda")
-    ctx.reduce("f32", n, 1, prog, ops, sc, "ACCU", r)
+    res = _shard_consistency(coot, ctx, "f32", prog, ops, sc, "ACCU", n)
+    out = None
+    if form == "c2_stored":
+        out = torch.empty(n, device="cuda")
+    elif form == "axpy_in_place":
+        out = ops[1]  # y = 2.5 x + y
+    ctx.reduce("f32", n, 1, prog, ops, sc, "ACCU", r, out)
     torch.cuda.synchronize()
     full = r[0].item()
-    res = _shard_consistency(coot, ctx, "f32", prog, ops, sc, "ACCU", n)
-    torch.cuda.synchronize()
     assert abs(res[0].item() - full) <= 1e-5 * abs(full)
-    s0, cnt = 5 << 26, 1 << 26
-    ctx.reduce("f32", cnt, 1, prog, [o[s0:s0 + cnt] for o in ops], sc, "ACCU", r)
-    torch.cuda.synchronize()
-    want, _ = oracle.run_chunked("f32", prog, ["randu"] * k, start=s0, count=cnt, scalars=sc,
-                                 kind="ACCU")
-    assert_reduction(r[0].item(), want, "f32", "ACCU")
+    del ops
+    want = _oracle_full("f32", prog, k, n, sc, "ACCU", out=out)
+    assert_reduction(full, want, "f32", "ACCU")

@@ -64,3 +64,35 @@ def test_invariant_totals_agree():
     t0 = float(oracle.reduce("f64", "ACCU", oracle.sum_dim("f64", 0, X, m, n)))
     t1 = float(oracle.reduce("f64", "ACCU", oracle.sum_dim("f64", 1, X, m, n)))
     assert abs(t0 - t) <= 1e-12 * t and abs(t1 - t) <= 1e-12 * t
+
+
+@pytest.mark.parametrize("etype", ["f32", "f64", "u32", "s64", "bf16", "f16", "e4m3", "e5m2"])
+def test_row_sums_fed_in_blocks_match_one_shot(etype):
+    """RowSums (the resumable dim-1 state used for 32768^2 full-size checks) fed
+    column blocks and split row ranges is bit-identical to one orc_sum_dim."""
+    m, n = 37, 53
+    X = oracle.fill(etype, "randu", m * n, stream=3)
+    want = oracle.sum_dim(etype, 1, X, m, n)
+    r = oracle.RowSums(etype, m)
+    cols = X.reshape(n, m)
+    for c0 in range(0, n, 10):
+        blk = cols[c0:c0 + 10].reshape(-1)
+        r.add_rows_of(blk, m, 0, 20)
+        r.add_rows_of(blk, m, 20, m - 20)
+    assert r.final().tobytes() == want.tobytes()
+
+
+def test_stream_chunks_match_run_chunked():
+    """stream_chunks (threaded, in-order) == one sequential run_chunked."""
+    from progs import C2
+    acc_want, z_want = oracle.run_chunked("f32", C2, ["randu"] * 3, start=1000, count=100003,
+                                          scalars=[3.0], kind="ACCU", want_out=True, chunk=4096)
+    acc = oracle.Accumulator("f32", "ACCU")
+    parts = []
+    for off, z in oracle.stream_chunks("f32", C2, ["randu"] * 3, start=1000, count=100003,
+                                       scalars=[3.0], chunk=7777, threads=4):
+        assert off == sum(p.size for p in parts)
+        acc.add(z)
+        parts.append(z)
+    assert np.concatenate(parts).tobytes() == z_want.tobytes()
+    assert acc.final() == acc_want
