@@ -60,7 +60,8 @@ _lib = None
 def lib():
     global _lib
     if _lib is None:
-        path = _build.build()
+        # ORACLE_LIB_PATH: a prebuilt variant (the sanitizer build of tests/test_sanitizers.py)
+        path = os.environ.get("ORACLE_LIB_PATH") or _build.build()
         L = ctypes.CDLL(path)
         u64, i32, vp = ctypes.c_uint64, ctypes.c_int, ctypes.c_void_p
         L.orc_half_from_double.restype = ctypes.c_uint16

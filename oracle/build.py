@@ -10,19 +10,25 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 SRC = os.path.join(HERE, "coot_oracle.c")
 LIB = os.path.join(HERE, "liboracle.so")
+# AddressSanitizer + UndefinedBehaviorSanitizer build for tests/test_sanitizers.py
+LIB_SAN = os.path.join(HERE, "liboracle_san.so")
+SAN_FLAGS = ["-fsanitize=address,undefined", "-fno-sanitize-recover=undefined",
+             "-fno-omit-frame-pointer", "-g"]
 
 
-def build(force: bool = False) -> str:
-    if not force and os.path.exists(LIB) and os.path.getmtime(LIB) >= os.path.getmtime(SRC):
-        return LIB
+def build(force: bool = False, sanitize: bool = False) -> str:
+    lib = LIB_SAN if sanitize else LIB
+    if not force and os.path.exists(lib) and os.path.getmtime(lib) >= os.path.getmtime(SRC):
+        return lib
     cmd = [
         "gcc", "-std=gnu11", "-O2", "-ffp-contract=off", "-fno-fast-math",
         "-fexcess-precision=standard", "-fPIC", "-shared", "-Wall", "-Wextra",
-        "-Wno-unused-parameter", SRC, "-o", LIB + ".tmp", "-lquadmath", "-lm",
+        "-Wno-unused-parameter", *(SAN_FLAGS if sanitize else []), SRC, "-o", lib + ".tmp",
+        "-lquadmath", "-lm",
     ]
     subprocess.check_call(cmd)
-    os.replace(LIB + ".tmp", LIB)
-    return LIB
+    os.replace(lib + ".tmp", lib)
+    return lib
 
 
 if __name__ == "__main__":

@@ -34,10 +34,12 @@ FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-fmad=false",
          "-Xptxas", "-warn-spills"] + os.environ.get("COOT_EXTRA_FLAGS", "").split()
 
 
+# COOT_EXTRA_LDFLAGS: extra link flags (the sanitizer build, tests/test_sanitizers.py).
 # COOT_DEV_TYPES=f32[,f64...]: a development build with the kernels of the
 # listed element types only (the other types' launchers are stubs returning
 # cudaErrorNotSupported) — ~1/8 of the compile time, for kernel iteration.
 # Use it with COOT_LIB_NAME (a side-by-side library) and COOT_LIB_PATH.
+# COOT_DEV_TYPES=none: no kernels at all (the host runtime alone).
 _DEV_TYPES = [t for t in os.environ.get("COOT_DEV_TYPES", "").split(",") if t]
 _ALL_TYPES = {"f32": "float", "f64": "double", "u32": "uint32_t", "s64": "s64", "bf16": "bf16",
               "f16": "f16", "e4m3": "e4m3", "e5m2": "e5m2"}
@@ -139,7 +141,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
             list(ex.map(_compile, todo))
     objs = [_obj(s) for s in srcs]
     tmp = LIB + ".tmp"
-    subprocess.check_call([NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-Xcompiler", "-fPIC"])
+    subprocess.check_call([NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-Xcompiler", "-fPIC",
+                           *os.environ.get("COOT_EXTRA_LDFLAGS", "").split()])
     # the library is stamped as old as its oldest object, so a header edited
     # during this build still makes up_to_date() false next time
     oldest = min(os.path.getmtime(o) for o in objs)

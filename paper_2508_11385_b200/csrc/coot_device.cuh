@@ -712,6 +712,13 @@ __device__ __forceinline__ void un_vec(T (&v)[W]) {
     // elements per dispatch next to its register stack).
     constexpr int G = W < GMAX ? W : GMAX;
     static_assert(W % G == 0, "group size");
+#ifdef COOT_EXPERIMENT_EXPF  // A/B experiment only (not correctly rounded): the cost of CR
+    if constexpr (std::is_same<T, float>::value) {
+#pragma unroll
+      for (int w = 0; w < W; ++w) v[w] = (OP == COOT_OP_EXP) ? expf(v[w]) : logf(v[w]);
+      return;
+    }
+#endif
 #pragma unroll
     for (int g = 0; g < W; g += G) {
       T x[G];

@@ -9,6 +9,7 @@
 // host-only and happens before anything is enqueued.
 #include <cuda_runtime.h>
 #include <dlfcn.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include <algorithm>
 #include <cstdarg>
@@ -22,6 +23,17 @@
 #include "coot_internal.h"
 
 using coot::u64;
+
+// One NVTX range per compute entry point (named after the coot_* call), so a
+// profiler timeline (nsys / ncu --nvtx) attributes every launch to the call
+// that made it.  NVTX v3 is header-only: without an attached tool each push /
+// pop is a test of a null function pointer.
+namespace {
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+}  // namespace
 
 // ---- NCCL, loaded at first use (coot_comm_*) ---------------------------------
 // The types and the calls below are NCCL's public C API as declared in nccl.h
@@ -1147,12 +1159,14 @@ coot_status coot_set_stream(coot_ctx* ctx, void* cuda_stream) {
 }
 
 coot_status coot_eval(coot_ctx* ctx, const coot_expr* e, void* out) {
+  NvtxRange nvtx_("coot_eval");
   if (!e) return fail(COOT_ERR_CONTRACT, "contract: expression descriptor is NULL");
   const coot_operand outv = dense_view(out, e->n_rows, e->n_cols);
   return eval_common(ctx, e, &outv);
 }
 
 coot_status coot_eval_view(coot_ctx* ctx, const coot_expr* e, const coot_operand* out) {
+  NvtxRange nvtx_("coot_eval_view");
   if (!out) return fail(COOT_ERR_CONTRACT, "contract: out view is NULL");
   return eval_common(ctx, e, out);
 }
@@ -1162,12 +1176,14 @@ static coot_status reduce_comm(coot_ctx* ctx, const coot_expr* e, uint32_t kind,
 
 coot_status coot_reduce(coot_ctx* ctx, const coot_expr* e, uint32_t kind, void* result,
                         void* out_or_null) {
+  NvtxRange nvtx_("coot_reduce");
   if (ctx && ctx->comm) return reduce_comm(ctx, e, kind, result, out_or_null);
   return reduce_common(ctx, e, kind, result, out_or_null, coot::FINAL_ROUND);
 }
 
 coot_status coot_reduce_partial(coot_ctx* ctx, const coot_expr* e, uint32_t kind, void* partial,
                                 void* out_or_null) {
+  NvtxRange nvtx_("coot_reduce_partial");
   return reduce_common(ctx, e, kind, partial, out_or_null, coot::FINAL_PARTIAL);
 }
 
@@ -1230,6 +1246,7 @@ coot_status coot_mailbox_destroy(coot_ctx* ctx, void* mailbox) {
 coot_status coot_reduce_exchange(coot_ctx* ctx, const coot_expr* e, uint32_t kind,
                                  void* const* mailboxes, uint32_t nranks, uint32_t rank,
                                  uint64_t epoch, void* result, void* out_or_null) {
+  NvtxRange nvtx_("coot_reduce_exchange");
   coot_status st = check_ctx(ctx);
   if (st != COOT_OK) return st;
   if (kind == COOT_RED_SUM_DIM0 || kind == COOT_RED_SUM_DIM1)
@@ -1261,6 +1278,7 @@ coot_status coot_partial_bytes(uint32_t kind, uint64_t len, uint64_t* bytes) {
 
 coot_status coot_combine(coot_ctx* ctx, uint32_t elem, uint32_t kind, const void* partials,
                          uint32_t nparts, uint64_t len, void* result) {
+  NvtxRange nvtx_("coot_combine");
   coot_status st = check_ctx(ctx);
   if (st != COOT_OK) return st;
   if (elem_size(elem) == 0) return fail(COOT_ERR_CONTRACT, "contract: unknown element type %u", elem);
@@ -1451,6 +1469,7 @@ coot_status coot_shard_range(uint64_t n, uint32_t rank, uint32_t nranks, uint64_
 coot_status coot_fill(coot_ctx* ctx, uint32_t elem, uint32_t fill_kind, uint64_t seed,
                       uint64_t stream, uint64_t start, uint64_t count, uint64_t n_rows,
                       uint64_t k, void* out) {
+  NvtxRange nvtx_("coot_fill");
   coot_status st = check_ctx(ctx);
   if (st != COOT_OK) return st;
   if (elem_size(elem) == 0) return fail(COOT_ERR_CONTRACT, "contract: unknown element type %u", elem);
@@ -1480,6 +1499,7 @@ coot_status coot_fill(coot_ctx* ctx, uint32_t elem, uint32_t fill_kind, uint64_t
 
 coot_status coot_stream_mix(coot_ctx* ctx, uint32_t n_read, uint32_t n_write, uint64_t n,
                             const void* const* in, void* out, void* sink) {
+  NvtxRange nvtx_("coot_stream_mix");
   coot_status st = check_ctx(ctx);
   if (st != COOT_OK) return st;
   if (n_read > 3 || n_write > 1 || n_read + n_write == 0)
@@ -1506,6 +1526,7 @@ coot_status coot_stream_mix(coot_ctx* ctx, uint32_t n_read, uint32_t n_write, ui
 }
 
 coot_status coot_sync(coot_ctx* ctx) {
+  NvtxRange nvtx_("coot_sync");
   coot_status st = check_ctx(ctx);
   if (st != COOT_OK) return st;
   cudaError_t e = cudaStreamSynchronize(ctx->stream);

@@ -14,6 +14,8 @@ C2 = [("LOAD", 0), ("LOAD", 1), ("MUL", 0), ("EXP", 0), ("SCALAR", 0), ("LOAD", 
 AXPY = [("SCALAR", 0), ("LOAD", 0), ("MUL", 0), ("LOAD", 1), ("ADD", 0)]
 DOT = [("LOAD", 0), ("LOAD", 1), ("MUL", 0)]
 CONFIGS = [(0, 0, 2), (512, 96, 2), (0, 0, 2), (512, 96, 2), (1024, 64, 2), (0, 0, 2)]
+if len(sys.argv) > 1:  # tile,kb,ctas ...
+    CONFIGS = [tuple(int(v) for v in c.split(",")) for c in sys.argv[1:]]
 
 
 def mkctx(tile, kb, ctas):
@@ -55,16 +57,24 @@ def main():
     base = coot.Context(0)
     for s, t in enumerate(a + [x, y]):
         base.fill(t, "randu", stream=s)
-    for tile, kb, ctas in CONFIGS:
-        ctx = mkctx(tile, kb, ctas)
-        t_c2 = timed(lambda: ctx.reduce("f32", n1, 1, C2, a, [3.0], "ACCU", r, z))
-        t_ro = timed(lambda: ctx.reduce("f32", n1, 1, C2, a, [3.0], "ACCU", r))
-        t_ax = timed(lambda: ctx.reduce("f32", n2, 1, AXPY, [x, y], [2.5], "ACCU", r, y), 10)
-        t_dot = timed(lambda: ctx.reduce("f32", n2, 1, DOT, [x, y], [], "ACCU", r), 10)
-        t_acc = timed(lambda: ctx.reduce("f32", n2, 1, [("LOAD", 0)], [x], [], "ACCU", r), 10)
-        print(f"tile={tile:5d} kb={kb:3d} ctas={ctas}  c2 eval+accu {16 * n1 / t_c2 / 1e6:7.1f}"
-              f"  c2 reduce {12 * n1 / t_ro / 1e6:7.1f}  axpy {12 * n2 / t_ax / 1e6:7.1f}"
-              f"  dot {8 * n2 / t_dot / 1e6:7.1f}  accu {4 * n2 / t_acc / 1e6:7.1f} GB/s", flush=True)
+    ctxs = [mkctx(*c) for c in CONFIGS]
+    rounds = int(os.environ.get("TUNE_ROUNDS", "3"))
+    res = {}
+    for rnd in range(rounds):  # interleaved rounds: clock / power drift hits every config alike
+        for c, ctx in zip(CONFIGS, ctxs):
+            t_c2 = timed(lambda: ctx.reduce("f32", n1, 1, C2, a, [3.0], "ACCU", r, z), 400)
+            t_ro = timed(lambda: ctx.reduce("f32", n1, 1, C2, a, [3.0], "ACCU", r), 400)
+            t_ax = timed(lambda: ctx.reduce("f32", n2, 1, AXPY, [x, y], [2.5], "ACCU", r, y), 50)
+            t_dot = timed(lambda: ctx.reduce("f32", n2, 1, DOT, [x, y], [], "ACCU", r), 50)
+            t_acc = timed(lambda: ctx.reduce("f32", n2, 1, [("LOAD", 0)], [x], [], "ACCU", r), 50)
+            res.setdefault(c, []).append((16 * n1 / t_c2 / 1e6, 12 * n1 / t_ro / 1e6,
+                                          12 * n2 / t_ax / 1e6, 8 * n2 / t_dot / 1e6,
+                                          4 * n2 / t_acc / 1e6))
+    for (tile, kb, ctas), v in res.items():
+        med = [sorted(col)[len(col) // 2] for col in zip(*v)]
+        print(f"tile={tile:5d} kb={kb:3d} ctas={ctas}  c2 eval+accu {med[0]:7.1f}"
+              f"  c2 reduce {med[1]:7.1f}  axpy {med[2]:7.1f}  dot {med[3]:7.1f}  accu {med[4]:7.1f}"
+              f" GB/s (median of {len(v)})", flush=True)
 
 
 if __name__ == "__main__":
