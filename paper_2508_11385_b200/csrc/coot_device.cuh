@@ -607,8 +607,7 @@ __device__ __forceinline__ void half_round_vec(const float (&y)[W], H (&v)[W]) {
     } else {
       asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(p) : "f"(y[w + 1]), "f"(y[w]));
     }
-    v[w] = H((unsigned short)(p & 0xffffu), true);
-    v[w + 1] = H((unsigned short)(p >> 16), true);
+    memcpy(&v[w], &p, 4);  // the pair as one 32-bit register (no repacking)
   }
   if constexpr (W & 1) v[W - 1] = half_from_f32<H>(y[W - 1]);
 }
@@ -637,10 +636,14 @@ template <int OP, class H, int W>
 __device__ __forceinline__ void half2_vec(H (&a)[W], const H (&b)[W]) {
 #pragma unroll
   for (int w = 0; w + 1 < W; w += 2) {
-    const uint32_t d = half2_op<OP, H>((uint32_t)a[w].bits | ((uint32_t)a[w + 1].bits << 16),
-                                       (uint32_t)b[w].bits | ((uint32_t)b[w + 1].bits << 16));
-    a[w] = H((unsigned short)(d & 0xffffu), true);
-    a[w + 1] = H((unsigned short)(d >> 16), true);
+    // (a[w], a[w+1]) read / written as one 32-bit register: element w in the
+    // low half, as loaded from memory — a shift-and-or repack here made ptxas
+    // emit two byte permutes per pair that it could not fold away
+    uint32_t x, y;
+    memcpy(&x, &a[w], 4);
+    memcpy(&y, &b[w], 4);
+    const uint32_t d = half2_op<OP, H>(x, y);
+    memcpy(&a[w], &d, 4);
   }
   if constexpr (W & 1) a[W - 1] = half_bin<OP, H>(a[W - 1], b[W - 1]);
 }

@@ -129,6 +129,50 @@ struct StaticStep {
   }
 };
 
+// ---- fp8 storage, catalog c2 (exp(A % B) + s*C): cheap EXP, verified ------
+// R25 makes an fp8 program an f32 program whose FINAL value is rounded once
+// to the 8-bit format.  For c2 the device may therefore evaluate EXP with the
+// cheap CUDA expf (<= 2 ulp) instead of the correctly rounded f32 EXP (R6) as
+// long as the final 8-bit result provably cannot differ.  With E = RN32(e^x)
+// (the exact program's node) and E' = expf(x): |E' - E| <= 2.5 ulp(E'), and
+// the exact z = RN32(E + t), the fast z' = RN32(E' + t) (t = RN32(s C), any
+// sign) differ by at most D0 = |E' - E| + 2 ulp(z') <= |E'| 2^-21 + |z'| 2^-22.
+// The test brackets z' by lo = RN32(z' - D), hi = RN32(z' + D) with D = 2 D0
+// (covers the half-ulp rounding of lo / hi) and narrows both: RN8 (saturating)
+// is monotone, so if RN8(lo) == RN8(hi) (same byte), RN8(z) is that byte.
+// x = A % B = 0 gives E' = E = 1 exactly: D = 0.  Undecided (a bracket that
+// straddles an 8-bit rounding boundary, or a non-finite E'): the whole
+// dispatch is recomputed with the exact program.
+// the exact program over the whole dispatch (the rare undecided case):
+// operands reloaded from the source, the correctly rounded f32 EXP (R6)
+template <class T, int W, class Src>
+__device__ __noinline__ void fp8_c2_exact(const Src& src, float sc, float (&z)[W]) {
+  float y[W];
+  load_to<T, W>(src, 0, z);
+  load_to<T, W>(src, 1, y);
+#pragma unroll 1
+  for (int w = 0; w < W; ++w) z[w] = crm::cr_expf(bin<COOT_OP_MUL>(z[w], y[w]));
+  load_to<T, W>(src, 2, y);
+#pragma unroll 1
+  for (int w = 0; w < W; ++w) z[w] = bin<COOT_OP_ADD>(z[w], bin<COOT_OP_MUL>(sc, y[w]));
+}
+template <int... Code>
+struct IsC2 {
+  static constexpr bool value = false;
+};
+template <>
+struct IsC2<COOT_OP_LOAD << 4, (COOT_OP_LOAD << 4) | 1, COOT_OP_MUL << 4, COOT_OP_EXP << 4,
+            COOT_OP_SCALAR << 4, (COOT_OP_LOAD << 4) | 2, COOT_OP_MUL << 4, COOT_OP_ADD << 4> {
+  static constexpr bool value = true;
+};
+template <int... Code>
+constexpr bool is_c2_prog() {
+  return IsC2<Code...>::value;
+}
+#ifndef COOT_FP8_FAST_EXP
+#define COOT_FP8_FAST_EXP 1
+#endif
+
 template <class Prog>
 struct CatalogEval;
 template <int... Code>
@@ -140,9 +184,57 @@ struct CatalogEval<StaticProg<Code...>> {
   static constexpr bool kIdentity = sizeof...(Code) == 1 && StaticProg<Code...>::codes[0] == 0;
   template <class T, int W, class Src>
   __device__ __forceinline__ static void eval_src(const Src& src, const FusedArgs& a, T (&out)[W]) {
-    typename ComputeT<T>::type st[COOT_MAX_STACK][W];
-    StaticStep<T, W, 0, Code...>::run(st, src, a);
-    narrow_vec<T, W>(st[0], out);
+    if constexpr (COOT_FP8_FAST_EXP && is_fp8<T>() && is_c2_prog<Code...>()) {
+      float z[W], y[W];
+      load_to<T, W>(src, 0, z);
+      load_to<T, W>(src, 1, y);
+#pragma unroll
+      for (int w = 0; w < W; ++w) z[w] = bin<COOT_OP_MUL>(z[w], y[w]);
+      load_to<T, W>(src, 2, y);
+      const float sc = scalar_as<float>(a.scalars[0]);
+      float lo[W], hi[W];
+#pragma unroll
+      for (int w = 0; w < W; ++w) {
+        const float e0 = expf(z[w]);
+        // x == 0: E' = 1 exactly and D = 0; else D = 2 (|E'| 2^-21 + |z'| 2^-22).
+        // Selects in PTX: ptxas otherwise branches around the expf.
+        const float x = z[w];
+        float e, D;
+        asm("{ .reg .pred p; setp.eq.f32 p, %2, 0f00000000; selp.f32 %0, 0f3F800000, %1, p; }"
+            : "=f"(e) : "f"(e0), "f"(x));
+        z[w] = bin<COOT_OP_ADD>(e, bin<COOT_OP_MUL>(sc, y[w]));
+        const float Dv = __fmaf_rn(fabsf(e0), 0x1p-20f, fabsf(z[w]) * 0x1p-21f);
+        asm("{ .reg .pred p; setp.eq.f32 p, %2, 0f00000000; selp.f32 %0, 0f00000000, %1, p; }"
+            : "=f"(D) : "f"(Dv), "f"(x));
+        lo[w] = __fsub_rn(z[w], D);
+        hi[w] = __fadd_rn(z[w], D);
+      }
+      T nlo[W], nhi[W];
+      narrow_vec<T, W>(lo, nlo);
+      narrow_vec<T, W>(hi, nhi);
+      uint32_t diff = 0;
+#pragma unroll
+      for (int w = 0; w + 3 < W; w += 4) {
+        uint32_t a4, b4;
+        memcpy(&a4, &nlo[w], 4);
+        memcpy(&b4, &nhi[w], 4);
+        diff |= a4 ^ b4;
+      }
+#pragma unroll
+      for (int w = W & ~3; w < W; ++w) diff |= (uint32_t)(nlo[w].bits ^ nhi[w].bits);
+      const bool ok = diff == 0;
+      if (__builtin_expect(!ok, 0)) {
+        float r[W];  // a local copy: only the rare branch touches memory
+        fp8_c2_exact<T, W>(src, sc, r);
+        narrow_vec<T, W>(r, nlo);
+      }
+#pragma unroll
+      for (int w = 0; w < W; ++w) out[w] = nlo[w];
+    } else {
+      typename ComputeT<T>::type st[COOT_MAX_STACK][W];
+      StaticStep<T, W, 0, Code...>::run(st, src, a);
+      narrow_vec<T, W>(st[0], out);
+    }
   }
   template <class T, int W>
   __device__ __forceinline__ static void eval(const T (&in)[K][W], const FusedArgs& a, T (&out)[W]) {

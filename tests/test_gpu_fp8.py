@@ -170,3 +170,20 @@ def test_builder_and_view(ctxs):
     zz[diag] = oracle.eval_program("e4m3", P("L0 S0 ADD"), [z[diag]], [400.0])
     assert np.array_equal(to_host(Z.data, "e4m3"), zz)
     assert np.all(oracle.to_float("e4m3", zz[diag]) <= 448.0)
+
+
+@pytest.mark.parametrize("etype", FP8)
+@pytest.mark.parametrize("scalar", [3.0, -1.5, 0.0078125])
+def test_c2_every_input_triple(ctxs, etype, scalar):
+    """Catalog c2 (exp(A % B) + s*C) on EVERY (a, b, c) triple of 8-bit patterns
+    (2^24 elements, NaNs included): the fast path (cheap expf + a proof that the
+    8-bit rounding cannot change, exact program otherwise) is bit-identical to
+    the oracle's exact f32 program + one rounding, on the catalog kernel and on
+    the interpreter; the accu of Z too."""
+    i = np.arange(1 << 24, dtype=np.uint32)
+    a, b, c = (i & 255).astype(np.uint8), ((i >> 8) & 255).astype(np.uint8), (i >> 16).astype(np.uint8)
+    prog = P(CATALOG[2])
+    want = oracle.eval_program(etype, prog, [a, b, c], [scalar])
+    for name, ctx in ctxs.items():
+        res, z = run(ctx, etype, prog, [a, b, c], [scalar], kind="MINMAX")
+        same_bits(etype, z, want)
