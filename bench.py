@@ -409,7 +409,56 @@ def measure_scaling_configs(coot, ctx, comm_ctx, mailbox, rank, world, dist, dev
         out.append(rec)
         del ops, z, lw
         torch.cuda.empty_cache()
+    out.append(measure_c3_dim1_scaling(coot, ctx, comm_ctx, mailbox, rank, world, dist, dev))
     return out
+
+
+C3_ROWS = C3_COLS = 32768
+
+
+def measure_c3_dim1_scaling(coot, ctx, comm_ctx, mailbox, rank, world, dist, dev):
+    """BASELINE configs[2] at N > 1: sum(X,1) of the 32768 x 32768 f64 Mat, strong-
+    scaled over column blocks (each rank sums its columns for every row; the
+    n_rows partial vectors are exchanged and combined in rank order).  Transports:
+    the in-kernel vector exchange (one dim-1 kernel per rank, partial vectors
+    stored into every rank's mailbox over NVLink) and libcoot's NCCL
+    communicator (partial kernel -> ncclAllGather -> combine kernel)."""
+    import torch
+    from paper_2508_11385_b200.dist import column_block
+    m, ncols = C3_ROWS, C3_COLS
+    c0, c1 = column_block(ncols, rank, world)
+    X = torch.empty(m * (c1 - c0), dtype=torch.float64, device=dev)
+    ctx.fill(X, "randu", stream=0, start=c0 * m, n_rows=m)
+    lw = coot.lower(coot.Mat(X, m, c1 - c0))
+    rec = {"config": "c3 sum(X,1), 32768^2 f64, column blocks", "global_elements": m * ncols}
+    results = {}
+    transports = []
+    if comm_ctx is not None:
+        res_c = torch.zeros(m, dtype=torch.float64, device=dev)
+        transports.append(("nccl", lambda: comm_ctx.reduce("f64", m, c1 - c0, lw.program, lw.operands,
+                                                           [], "SUM_DIM1", res_c), lambda: res_c))
+    if mailbox is not None and mailbox.vec_capacity >= m:
+        box = {}
+        transports.append(("mailbox", lambda: box.__setitem__("r", mailbox.sum_dim1(lw)),
+                           lambda: box["r"]))
+    for tname, call, get in transports:
+        dist.barrier()
+        torch.cuda.synchronize()
+        ms, reps = time_calls(call, ctx.stream)
+        tt = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        ms = float(tt[0])
+        rec[tname] = {"ms": ms, "reps": reps, "GBps": m * ncols * 8 / (ms * 1e-3) / 1e9}
+        results[tname] = get().clone()
+    if len(results) == 2:
+        a_, b_ = results.values()
+        rec["transports_bit_identical"] = bool(torch.equal(a_, b_))
+    best = min((rec[t]["ms"] for t, _, _ in transports), default=None)
+    if best:
+        rec["GBps"] = m * ncols * 8 / (best * 1e-3) / 1e9
+    del X, lw
+    torch.cuda.empty_cache()
+    return rec
 
 
 def cpu_baseline_oracle(n=M_ROWS * N_COLS, what="full c2 workload on rank 0's block"):
@@ -557,7 +606,11 @@ def main():
     # libcoot), or torch.distributed's all-gather between the two libcoot
     # kernels (DistReducer; the host-staged path under gloo)
     exchange = os.environ.get("COOT_BENCH_EXCHANGE", "mailbox")
-    mailbox = cdist.MailboxExchange.try_create(ctx) if multi else None
+    # the in-kernel mailbox exchange makes each rank's kernel wait for its
+    # peers: never with several ranks on one GPU (nothing runs those launches
+    # at the same time), so the shared-GPU dry run uses the host-staged path
+    mailbox = (cdist.MailboxExchange.try_create(ctx, vec_capacity=C3_ROWS)
+               if multi and not share else None)
     comm_ctx = None
     if multi and not share:
         uid = [coot.Context.comm_unique_id() if rank == 0 else None]

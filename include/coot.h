@@ -306,6 +306,34 @@ coot_status coot_reduce_exchange(coot_ctx* ctx, const coot_expr* e, uint32_t kin
                                  void* const* mailboxes, uint32_t nranks, uint32_t rank,
                                  uint64_t epoch, void* result, void* out_or_null);
 
+/* In-kernel exchange of sum(X,1) partial VECTORS (SURVEY.md:847-851;
+ * Armadillo sum(X,1) = row sums, R3): X is sharded by COLUMN blocks (every
+ * rank holds all n_rows rows of some columns), so each rank's row sums are
+ * partials of the global ones.
+ *
+ * coot_vec_mailbox_create: like coot_mailbox_create, for vectors of up to
+ *   `capacity` rows (1..2^32): 256 + 2 * COOT_MAX_RANKS * capacity * 8 bytes,
+ *   zeroed.  Map peers' with coot_mailbox_open, release with
+ *   coot_mailbox_close / coot_mailbox_destroy.
+ * coot_sum_dim_exchange: kind must be COOT_RED_SUM_DIM1; `e` is this rank's
+ *   column block (dense operands, n_rows <= capacity, the same n_rows on every
+ *   rank; n_cols may be 0); `result` receives the GLOBAL row sums (n_rows
+ *   eT values, f32 for the 8-bit types), identical bits on every rank and to
+ *   the host-staged coot_reduce_partial -> all-gather -> coot_combine path.
+ *   ONE kernel per rank: the CTA that finishes a tile of rows stores its
+ *   unrounded 8-byte partials into every rank's mailbox (NVLink P2P stores);
+ *   the CTA that completes the last of this rank's rows raises this rank's
+ *   flag in every mailbox, waits for all nranks flags in its own and combines
+ *   the nranks vectors in rank order 0..nranks-1, rounding once.  Epoch,
+ *   matching-call and timeout rules as for coot_reduce_exchange (a missing
+ *   rank makes the others fault after ~20 s).  `mailboxes` is a HOST array of
+ *   nranks device pointers as mapped in this process. */
+coot_status coot_vec_mailbox_create(coot_ctx* ctx, uint64_t capacity, void** mailbox,
+                                    void* ipc_handle);
+coot_status coot_sum_dim_exchange(coot_ctx* ctx, const coot_expr* e, uint32_t kind,
+                                  void* const* mailboxes, uint32_t nranks, uint32_t rank,
+                                  uint64_t epoch, uint64_t capacity, void* result);
+
 /* Synthetic inputs (fill::randu, and structured fills for closed
  * forms): out[i] = f(global index start+i) of an operand with n_rows rows,
  * stream = operand index, using the counter-based SplitMix64 recipe of

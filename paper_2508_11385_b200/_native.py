@@ -108,6 +108,9 @@ _SIGS = {
     "coot_mailbox_destroy": (_i32, [_vp, _vp]),
     "coot_reduce_exchange": (_i32, [_vp, ctypes.POINTER(Expr), _u32, ctypes.POINTER(_vp), _u32,
                                     _u32, _u64, _vp, _vp]),
+    "coot_vec_mailbox_create": (_i32, [_vp, _u64, ctypes.POINTER(_vp), _vp]),
+    "coot_sum_dim_exchange": (_i32, [_vp, ctypes.POINTER(Expr), _u32, ctypes.POINTER(_vp), _u32,
+                                     _u32, _u64, _u64, _vp]),
 }
 MAX_RANKS = 8
 IPC_HANDLE_BYTES = 64

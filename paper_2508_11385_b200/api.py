@@ -140,6 +140,22 @@ class Context:
         check(lib.coot_mailbox_create(self.handle, ctypes.byref(p), h))
         return int(p.value), h.raw
 
+    def vec_mailbox_create(self, capacity: int) -> tuple[int, bytes]:
+        """A zeroed vector mailbox for sum(X,1) partials of up to `capacity` rows:
+        (device pointer, CUDA IPC handle)."""
+        p = ctypes.c_void_p()
+        h = ctypes.create_string_buffer(N.IPC_HANDLE_BYTES)
+        check(lib.coot_vec_mailbox_create(self.handle, capacity, ctypes.byref(p), h))
+        return int(p.value), h.raw
+
+    def sum_dim_exchange(self, elem, n_rows, n_cols, program, operands, scalars, kind,
+                         mailboxes, rank: int, epoch: int, capacity: int, result: torch.Tensor):
+        e = N.make_expr(elem, n_rows, n_cols, program, operands, scalars)
+        mb = (ctypes.c_void_p * len(mailboxes))(*mailboxes)
+        check(lib.coot_sum_dim_exchange(self.handle, ctypes.byref(e), N.KIND[kind], mb,
+                                        len(mailboxes), rank, epoch, capacity,
+                                        ctypes.c_void_p(result.data_ptr())))
+
     def mailbox_open(self, ipc_handle: bytes) -> int:
         p = ctypes.c_void_p()
         h = ctypes.create_string_buffer(bytes(ipc_handle), N.IPC_HANDLE_BYTES)

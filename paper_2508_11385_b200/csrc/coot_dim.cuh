@@ -30,13 +30,104 @@ struct DimArgs {
   uint32_t nrt;         // dim1: row tiles
   uint32_t cg;          // dim1 TMA: columns per pipeline stage
   uint32_t dim;         // strided kernel: 0 or 1
+  u64 vcap;             // FINAL_EXCHANGE (sum(X,1) over column shards): rows per
+                        // vector-mailbox slot; the mailboxes are f.ex.mbox[]
 };
 
+// ---- in-kernel exchange of sum(X,1) partial vectors (FINAL_EXCHANGE) -------
+// Column shards of a Mat: every rank holds all n_rows of some columns, so each
+// rank's row sums are partials of the global ones.  Vector mailbox of a rank
+// (coot_vec_mailbox_create): u64 flag[MAX_RANKS] at 0, u64 tag[2][MAX_RANKS]
+// at 64 (epoch of each slot), S data[2][MAX_RANKS][vcap] at 256; half =
+// epoch & 1 (double-buffered like the record mailboxes, §7).
+//  1. every finisher of a row tile (the CTA that rounds its rows in the
+//     single-GPU kernel) instead stores its rows' unrounded S partials into
+//     data[half][rank][row] of EVERY rank's mailbox (NVLink P2P stores);
+//  2. it then adds its row count to a ticket; the CTA completing the m rows
+//     of this rank (all tiles published) tags and flags every mailbox and waits
+//     for every rank's flag in its own — nothing else of this rank is still
+//     running, so the wait cannot hold up this rank's own work;
+//  3. that CTA combines the P vectors in rank order 0..P-1 (the same S sum as
+//     coot_combine's combine_vec_kernel) and rounds once: identical bits on
+//     every rank and to the host-staged partial -> all-gather -> combine path.
+constexpr u64 kVecMboxHeader = 256;
+template <class T>
+__device__ __forceinline__ void publish_dim_value(const DimArgs& d, u64 idx,
+                                                  typename SumT<T>::type s) {
+  typedef typename SumT<T>::type S;
+  const Exchange& ex = d.f.ex;
+  const u64 off = ((ex.epoch & 1ull) * COOT_MAX_RANKS + ex.rank) * d.vcap + idx;
+  for (uint32_t p = 0; p < ex.nranks; ++p)
+    __stcg(reinterpret_cast<S*>(ex.mbox[p] + kVecMboxHeader) + off, s);
+}
+
+// The last of this rank's finishers (all m rows published): flags, wait,
+// rank-order combine of all rows by the NT threads of the calling group.
+template <class T, class Sync>
+__device__ void vec_exchange_finish(const DimArgs& d, uint32_t tid, uint32_t NT, Sync sync) {
+  typedef typename SumT<T>::type S;
+  typedef typename ResultT<T>::type R;
+  const Exchange& ex = d.f.ex;
+  const uint32_t P = ex.nranks;
+  const u64 half = (ex.epoch & 1ull) * COOT_MAX_RANKS;
+  if (tid == 0) {
+    __threadfence_system();  // this CTA's data stores (the others fenced before their ticket)
+    for (uint32_t p = 0; p < P; ++p)
+      __stcg(reinterpret_cast<unsigned long long*>(ex.mbox[p] + 64) + half + ex.rank, ex.epoch);
+    __threadfence_system();
+    for (uint32_t p = 0; p < P; ++p)
+      st_release_sys(reinterpret_cast<unsigned long long*>(ex.mbox[p]) + ex.rank, ex.epoch);
+    const unsigned long long* own = reinterpret_cast<const unsigned long long*>(ex.mbox[ex.rank]);
+    const unsigned long long t0 = globaltimer_ns();
+    for (uint32_t q = 0; q < P; ++q) {
+      while (ld_acquire_sys(own + q) < ex.epoch) {
+        __nanosleep(256);
+        if (globaltimer_ns() - t0 > 20000000000ull) __trap();  // a rank never arrived
+      }
+    }
+    for (uint32_t q = 0; q < P; ++q)  // every slot must hold this call's vector
+      if (__ldcg(own + 8 + half + q) != ex.epoch) __trap();
+    d.tickets[d.nrt] = 0u;  // self-reset for the next call
+  }
+  sync();
+  const S* data = reinterpret_cast<const S*>(ex.mbox[ex.rank] + kVecMboxHeader) + half * d.vcap;
+  for (u64 r = tid; r < d.m; r += NT) {
+    S tot = S(0);
+    for (uint32_t q = 0; q < P; ++q) tot = sum_add<S>(tot, __ldcg(data + (u64)q * d.vcap + r));
+    R v;
+    if constexpr (is_float<T>()) v = round_to<R>(tot);
+    else v = (R)tot;
+    reinterpret_cast<R*>(d.result)[r] = v;
+  }
+}
+
+// A finisher's rows are published: count them; the group completing the m
+// rows runs the exchange.  Called by every thread of the group (NT threads,
+// synchronised by `sync`); `flag` is a shared word of the group.
+template <class T, class Sync>
+__device__ __forceinline__ void vec_exchange_arrive(const DimArgs& d, u64 rows, uint32_t tid,
+                                                    uint32_t NT, bool* flag, Sync sync) {
+  __threadfence_system();  // this thread's remote stores before the ticket
+  sync();
+  if (tid == 0) {
+    const unsigned old = atomicAdd(&d.tickets[d.nrt], (unsigned)rows);
+    *flag = (u64)old + rows == d.m;
+  }
+  sync();
+  if (*flag) vec_exchange_finish<T>(d, tid, NT, sync);
+  sync();  // *flag is rewritten by the group's next call
+}
+
+template <class T>
+__device__ __forceinline__ void publish_dim_value(const DimArgs& d, u64 idx,
+                                                  typename SumT<T>::type s);
 template <class T>
 __device__ __forceinline__ void store_dim_value(const DimArgs& d, u64 idx,
                                                 typename SumT<T>::type s) {
   typedef typename SumT<T>::type S;
-  if (d.final_mode == FINAL_PARTIAL) {
+  if (d.final_mode == FINAL_EXCHANGE) {
+    publish_dim_value<T>(d, idx, s);
+  } else if (d.final_mode == FINAL_PARTIAL) {
     reinterpret_cast<S*>(d.result)[idx] = s;
   } else {
     typedef typename ResultT<T>::type R;  // f32 for the 8-bit storage types
@@ -326,6 +417,8 @@ __device__ __forceinline__ void dim1_body(const DimArgs& d) {
   auto row_of = [&](int w) -> u64 {
     return vec_rows ? r0 + (u64)q * W + w : r0 + q + (u64)w * tpr;
   };
+  auto block_sync = [] { __syncthreads(); };
+  const u64 tile_rows = (d.m - r0) < R ? (d.m - r0) : R;
   if (d.nchunks == 1) {
     if (g == 0) {
 #pragma unroll
@@ -334,6 +427,8 @@ __device__ __forceinline__ void dim1_body(const DimArgs& d) {
         if (r < d.m) store_dim_value<T>(d, r, acc[w]);
       }
     }
+    if (d.final_mode == FINAL_EXCHANGE)
+      vec_exchange_arrive<T>(d, tile_rows, threadIdx.x, kThreads, &last, block_sync);
     return;
   }
   S* part = reinterpret_cast<S*>(d.part);
@@ -365,6 +460,8 @@ __device__ __forceinline__ void dim1_body(const DimArgs& d) {
     }
   }
   if (threadIdx.x == 0) d.tickets[rt] = 0u;
+  if (d.final_mode == FINAL_EXCHANGE)
+    vec_exchange_arrive<T>(d, tile_rows, threadIdx.x, kThreads, &last, block_sync);
 }
 
 template <class T, class EV>

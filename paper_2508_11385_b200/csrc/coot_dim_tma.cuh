@@ -283,6 +283,8 @@ __global__ void __launch_bounds__(kTmaThreads, tma_min_ctas<EV>()) dim1_tma_kern
 #pragma unroll
         for (int w = 0; w < W; ++w) store_dim_value<T>(d, r0 + (u64)t * W + w, acc[w]);
       }
+      if (d.final_mode == FINAL_EXCHANGE)
+        vec_exchange_arrive<T>(d, nrows, t, kConsumerWarps * 32, &last, consumer_sync);
       continue;
     }
     S* part = reinterpret_cast<S*>(d.part);
@@ -306,6 +308,10 @@ __global__ void __launch_bounds__(kTmaThreads, tma_min_ctas<EV>()) dim1_tma_kern
         }
       }
       if (t == 0) d.tickets[rt] = 0u;
+      if (d.final_mode == FINAL_EXCHANGE) {
+        consumer_sync();  // every thread has read `last` before the arrive rewrites it
+        vec_exchange_arrive<T>(d, nrows, t, kConsumerWarps * 32, &last, consumer_sync);
+      }
     }
     consumer_sync();  // `last` is rewritten by the next piece
   }

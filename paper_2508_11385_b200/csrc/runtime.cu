@@ -121,6 +121,7 @@ struct coot_ctx {
   coot_stats_t stats{};
   bool log = false;
   const coot::Exchange* pending_ex = nullptr;  // set by coot_reduce_exchange for one call
+  uint64_t pending_vcap = 0;                   // coot_sum_dim_exchange: mailbox capacity
   cudaEvent_t handoff = nullptr;  // orders a new stream after the old one (coot_set_stream)
   // communicator (coot_comm_init): partial -> all-gather -> rank-order combine
   nccl::comm_t comm = nullptr;
@@ -789,7 +790,10 @@ coot_status run_dim(coot_ctx* ctx, const coot_expr* e, const Shape& sh, uint32_t
   const size_t sbytes = 8;  // f64 / u64 partial words
   const u64 nout = kind == COOT_RED_SUM_DIM0 ? n : m;
   const size_t obytes = final_mode == coot::FINAL_PARTIAL ? sbytes : result_elem_size(e->elem);
-  if (m == 0 || n == 0) {
+  const bool xchg = final_mode == coot::FINAL_EXCHANGE;  // sum(X,1), vector mailboxes
+  // a rank owning no columns still publishes a zero vector and combines: the
+  // LDG dim-1 kernel runs with empty column loops
+  if (m == 0 || (n == 0 && !xchg)) {
     if (nout) {
       cudaError_t ce = cudaMemsetAsync(result, 0, nout * obytes, ctx->stream);
       if (ce != cudaSuccess) return cuda_fail(ce, "cudaMemsetAsync");
@@ -818,8 +822,8 @@ coot_status run_dim(coot_ctx* ctx, const coot_expr* e, const Shape& sh, uint32_t
   // TMA-staged dim kernels: opt-in (COOT_DIM_TMA=1), and by default for
   // sum(X,1) of 4-byte types, the one case they measured faster than the LDG
   // kernels (f32 dim 1: 6.36 vs 5.74 TB/s at 32768^2; f64 / 16- / 8-bit slower)
-  const bool use_tma =
-      ctx->driver == 1 && (ctx->dim_tma || (kind == COOT_RED_SUM_DIM1 && es == 4));
+  const bool use_tma = ctx->driver == 1 && n > 0 &&
+                       (ctx->dim_tma || (kind == COOT_RED_SUM_DIM1 && es == 4));
   const u64 G = (u64)ctx->sm_count * ctx->tma_ctas_per_sm;  // TMA grid: persistent CTAs
   const u64 nk = e->n_operands;
   const u64 R1 = (u64)coot::kConsumerWarps * 32 * W;         // dim1 TMA rows per tile
@@ -912,8 +916,8 @@ coot_status run_dim(coot_ctx* ctx, const coot_expr* e, const Shape& sh, uint32_t
     const u64 tgt1 = es == 1 ? std::min<u64>(target, (u64)ctx->sm_count * 3) : target;
     u64 nchunks = std::max<u64>(1, tgt1 / nrt);
     nchunks = std::min<u64>(nchunks, std::max<u64>(1, n / (8 * Gc)));
-    const u64 ccols = ceil_div(n, nchunks);
-    nchunks = ceil_div(n, ccols);
+    const u64 ccols = std::max<u64>(1, ceil_div(n, nchunks));
+    nchunks = std::max<u64>(1, ceil_div(n, ccols));
     d.tpr = tpr;
     d.nrt = (uint32_t)nrt;
     d.ccols = ccols;
@@ -923,6 +927,12 @@ coot_status run_dim(coot_ctx* ctx, const coot_expr* e, const Shape& sh, uint32_t
       part_bytes = nchunks * m * sbytes;
       ntickets = nrt;
     }
+  }
+  if (xchg) {
+    // one more ticket (index nrt) counts the rows this rank has published
+    ntickets = std::max<size_t>(ntickets, (size_t)d.nrt + 1);
+    d.f.ex = *ctx->pending_ex;
+    d.vcap = ctx->pending_vcap;
   }
   coot_status st = grow_dim_scratch(ctx, part_bytes, ntickets);
   if (st != COOT_OK) return st;
@@ -1192,7 +1202,7 @@ coot_status coot_reduce_partial(coot_ctx* ctx, const coot_expr* e, uint32_t kind
 // flags only grow: each call raises them to its epoch).
 static const size_t kMailboxBytes = 4096;
 
-coot_status coot_mailbox_create(coot_ctx* ctx, void** mailbox, void* ipc_handle) {
+static coot_status mailbox_alloc(coot_ctx* ctx, size_t bytes, void** mailbox, void* ipc_handle) {
   coot_status st = check_ctx(ctx);
   if (st != COOT_OK) return st;
   if (!mailbox || !ipc_handle) return fail(COOT_ERR_CONTRACT, "contract: NULL argument");
@@ -1200,9 +1210,9 @@ coot_status coot_mailbox_create(coot_ctx* ctx, void** mailbox, void* ipc_handle)
   st = bind_device(ctx);
   if (st != COOT_OK) return st;
   void* p = nullptr;
-  cudaError_t ce = cudaMalloc(&p, kMailboxBytes);
+  cudaError_t ce = cudaMalloc(&p, bytes);
   if (ce != cudaSuccess) return cuda_fail(ce, "cudaMalloc(mailbox)");
-  ce = cudaMemset(p, 0, kMailboxBytes);
+  ce = cudaMemset(p, 0, bytes);
   if (ce == cudaSuccess) ce = cudaIpcGetMemHandle(reinterpret_cast<cudaIpcMemHandle_t*>(ipc_handle), p);
   if (ce != cudaSuccess) {
     cudaFree(p);
@@ -1210,6 +1220,21 @@ coot_status coot_mailbox_create(coot_ctx* ctx, void** mailbox, void* ipc_handle)
   }
   *mailbox = p;
   return ok();
+}
+
+coot_status coot_mailbox_create(coot_ctx* ctx, void** mailbox, void* ipc_handle) {
+  return mailbox_alloc(ctx, kMailboxBytes, mailbox, ipc_handle);
+}
+
+// Vector mailbox (sum(X,1) over column shards): flags, tags, then
+// 2 x COOT_MAX_RANKS slots of `capacity` 8-byte partial words (coot_dim.cuh).
+coot_status coot_vec_mailbox_create(coot_ctx* ctx, uint64_t capacity, void** mailbox,
+                                    void* ipc_handle) {
+  if (capacity == 0 || capacity > (1ull << 32))
+    return fail(COOT_ERR_BOUNDS, "bounds: vector mailbox capacity %llu (allowed 1..2^32)",
+                (unsigned long long)capacity);
+  return mailbox_alloc(ctx, (size_t)coot::kVecMboxHeader + 2ull * COOT_MAX_RANKS * capacity * 8,
+                       mailbox, ipc_handle);
 }
 
 coot_status coot_mailbox_open(coot_ctx* ctx, const void* ipc_handle, void** peer_mailbox) {
@@ -1266,6 +1291,41 @@ coot_status coot_reduce_exchange(coot_ctx* ctx, const coot_expr* e, uint32_t kin
   ctx->pending_ex = &ex;
   st = reduce_common(ctx, e, kind, result, out_or_null, coot::FINAL_EXCHANGE);
   ctx->pending_ex = nullptr;
+  return st;
+}
+
+coot_status coot_sum_dim_exchange(coot_ctx* ctx, const coot_expr* e, uint32_t kind,
+                                  void* const* mailboxes, uint32_t nranks, uint32_t rank,
+                                  uint64_t epoch, uint64_t capacity, void* result) {
+  NvtxRange nvtx_("coot_sum_dim_exchange");
+  coot_status st = check_ctx(ctx);
+  if (st != COOT_OK) return st;
+  if (kind != COOT_RED_SUM_DIM1)
+    return fail(COOT_ERR_CONTRACT,
+                "contract: the vector exchange covers sum(X,1) over column shards (SUM_DIM1) only");
+  if (!e) return fail(COOT_ERR_CONTRACT, "contract: expression descriptor is NULL");
+  if (!mailboxes || nranks == 0 || nranks > COOT_MAX_RANKS || rank >= nranks)
+    return fail(COOT_ERR_BOUNDS, "bounds: nranks %u / rank %u (max %d ranks)", nranks, rank,
+                COOT_MAX_RANKS);
+  if (epoch == 0) return fail(COOT_ERR_CONTRACT, "contract: epoch must be >= 1");
+  if (e->n_rows > capacity)
+    return fail(COOT_ERR_BOUNDS, "bounds: %llu rows exceed the vector mailbox capacity %llu",
+                (unsigned long long)e->n_rows, (unsigned long long)capacity);
+  if (any_strided(e, nullptr))
+    return fail(COOT_ERR_CONTRACT, "contract: the vector exchange takes dense operands only");
+  coot::Exchange ex{};
+  for (uint32_t p = 0; p < nranks; ++p) {
+    if (!mailboxes[p]) return fail(COOT_ERR_CONTRACT, "contract: mailbox %u is NULL", p);
+    ex.mbox[p] = reinterpret_cast<unsigned long long>(mailboxes[p]);
+  }
+  ex.epoch = epoch;
+  ex.nranks = nranks;
+  ex.rank = rank;
+  ctx->pending_ex = &ex;
+  ctx->pending_vcap = capacity;
+  st = reduce_common(ctx, e, kind, result, nullptr, coot::FINAL_EXCHANGE);
+  ctx->pending_ex = nullptr;
+  ctx->pending_vcap = 0;
   return st;
 }
 

@@ -110,36 +110,48 @@ class MailboxExchange:
     round trip, no collective call per reduction.  Same bits as DistReducer
     (same records, same rank-order combine)."""
 
-    def __init__(self, ctx: Context, group=None):
+    def __init__(self, ctx: Context, group=None, vec_capacity: int = 0):
+        """vec_capacity > 0 also sets up vector mailboxes for sum(X,1) over column
+        shards of up to that many rows (sum_dim1)."""
         self.ctx = ctx
         self.group = group
         self.world = dist.get_world_size(group)
         self.rank = dist.get_rank(group)
-        self.mine, handle = ctx.mailbox_create()
-        handles = [None] * self.world
-        dist.all_gather_object(handles, handle, group=group)
-        self.mailboxes, mapped = [], True
-        for r, h in enumerate(handles):
-            if r == self.rank:
-                self.mailboxes.append(self.mine)
-                continue
-            try:
-                self.mailboxes.append(ctx.mailbox_open(h))
-            except Exception:  # e.g. no peer access between these devices
-                self.mailboxes.append(None)
-                mapped = False
+        self.mine, self.mailboxes, ok = self._setup(ctx.mailbox_create())
+        self.vec_capacity = vec_capacity
+        self.vmine, self.vmailboxes = None, None
+        if vec_capacity > 0:
+            self.vmine, self.vmailboxes, vok = self._setup(ctx.vec_mailbox_create(vec_capacity))
+            ok = ok and vok
         oks = [None] * self.world
-        dist.all_gather_object(oks, mapped, group=group)
+        dist.all_gather_object(oks, ok, group=self.group)
         self.ok = all(oks)  # usable only if EVERY rank mapped every peer
         self.epoch = 0
+        self.vepoch = 0
         # no rank may release its mailbox while a peer could still write into it
         dist.barrier(group)
 
+    def _setup(self, created):
+        mine, handle = created
+        handles = [None] * self.world
+        dist.all_gather_object(handles, handle, group=self.group)
+        boxes, mapped = [], True
+        for r, h in enumerate(handles):
+            if r == self.rank:
+                boxes.append(mine)
+                continue
+            try:
+                boxes.append(self.ctx.mailbox_open(h))
+            except Exception:  # e.g. no peer access between these devices
+                boxes.append(None)
+                mapped = False
+        return mine, boxes, mapped
+
     @classmethod
-    def try_create(cls, ctx: Context, group=None):
+    def try_create(cls, ctx: Context, group=None, vec_capacity: int = 0):
         """Collective: a MailboxExchange if every rank could map every peer's
         mailbox, else None on every rank (the caller then uses DistReducer)."""
-        mx = cls(ctx, group)
+        mx = cls(ctx, group, vec_capacity)
         if mx.ok:
             return mx
         mx.close()
@@ -161,11 +173,27 @@ class MailboxExchange:
         self.epoch += 1
         return res
 
+    def sum_dim1(self, lw: Lowered) -> torch.Tensor:
+        """sum(X, 1) of a Mat sharded by column blocks (this rank's block `lw`):
+        the GLOBAL row sums on every rank, exchanged inside the dim-1 kernel
+        (coot_sum_dim_exchange).  Every rank must call it the same number of times."""
+        if not self.ok or not self.vec_capacity:
+            raise RuntimeError("MailboxExchange: no usable vector mailboxes (vec_capacity=0?)")
+        res = torch.empty(lw.n_rows, dtype=RESULT_DTYPE[lw.elem], device=self.ctx.device)
+        self.ctx.sum_dim_exchange(lw.elem, lw.n_rows, lw.n_cols, lw.program, lw.operands,
+                                  lw.scalars, "SUM_DIM1", self.vmailboxes, self.rank,
+                                  self.vepoch + 1, self.vec_capacity, res)
+        self.vepoch += 1
+        return res
+
     def close(self):
         torch.cuda.synchronize(self.ctx.device)
         dist.barrier(self.group)  # every rank's last kernel has finished writing
-        for r, p in enumerate(self.mailboxes):
-            if r != self.rank and p is not None:
-                self.ctx.mailbox_close(p)
+        for boxes in (self.mailboxes, self.vmailboxes or []):
+            for r, p in enumerate(boxes):
+                if r != self.rank and p is not None:
+                    self.ctx.mailbox_close(p)
         dist.barrier(self.group)
         self.ctx.mailbox_destroy(self.mine)
+        if self.vmine is not None:
+            self.ctx.mailbox_destroy(self.vmine)
