@@ -657,8 +657,12 @@ coot_status run_strided(coot_ctx* ctx, const coot_expr* e, const Shape& sh, int 
     a.nseg = (uint32_t)S;
     a.tile_units = (uint32_t)tu;
     a.stages = (uint32_t)stages;
-    a.producer_sleep = producer_sleep(ctx, e, -1);
     p.driver = 3;
+    // catalog programs take their own column-streaming instance (K1); others the
+    // interpreter (same arithmetic either way, K1 == K2 bitwise)
+    p.catalog = (ctx->flags & COOT_INIT_FORCE_INTERP) ? -1 : match_catalog(e);
+    if (acc >= coot::ACC_VAR && p.catalog > 0) p.catalog = -1;  // see pick_fused_acc
+    a.producer_sleep = producer_sleep(ctx, e, p.catalog);
     p.smem = pad_smem(ctx, (unsigned)(stages * stage_bytes + 16 * stages), ctx->tma_ctas_per_sm);
     p.grid = (unsigned)std::max<u64>(1, std::min<u64>(e->n_cols * S, G));
   }

@@ -179,3 +179,35 @@ def test_view_alias_rules(coot, ctx):
     # identical view in place is fine
     s = A.submat(3, 3, 40, 50)
     s *= 2
+
+
+@pytest.mark.parametrize("etype", ALL)
+@pytest.mark.parametrize("prog", ["S0 L0 MUL L1 ADD", "L0 L1 MUL EXP S0 L2 MUL ADD",
+                                  "L0 L1 MUL S0 L2 MUL ADD"])
+def test_column_views_catalog_equals_interpreter(coot, etype, prog):
+    """Column-streamed submatrix views: a catalog program's own instance (K1)
+    and the interpreter (K2) give the same bits, element-wise and reduced, and
+    match the oracle."""
+    from paper_2508_11385_b200 import _native as N
+    p = P(prog)
+    if etype in ("u32", "s64") and "EXP" in prog:
+        pytest.skip("EXP is float-only (R9)")
+    m, n = 2048, 96
+    mats = [dev_mat(coot, etype, m, n, 10 + k) for k in range(3)]
+    views = [M.submat(4, 2 + k, 4 + 1999, 2 + k + 80) for k, (M, _) in enumerate(mats)]
+    hs = [H[4:2004, 2 + k:83 + k].T.reshape(-1) for k, (_, H) in enumerate(mats)]  # 2000 x 81
+    k = 1 + max(a for o, a in p if o == "LOAD")
+    sc = [3] if etype in ("u32", "s64") else [2.5]
+    want = oracle.eval_program(etype, p, hs[:k], sc)
+    outs = []
+    for flags in (0, N.INIT_FORCE_INTERP):
+        c = coot.Context(0, flags=flags)
+        out = torch.empty(2000 * 81, dtype=TORCH[etype], device="cuda")
+        r = torch.zeros(2, dtype=TORCH[etype], device="cuda")
+        ops = [v.operand() for v in views[:k]]
+        c.reduce(etype, 2000, 81, p, ops, sc, "ACCU", r, out)
+        torch.cuda.synchronize()
+        outs.append((to_host(out, etype), to_host(r, etype)))
+    assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
+    assert np.array_equal(outs[0][0], want) if etype in ("u32", "s64") else \
+        np.array_equal(outs[0][0].view(np.uint8), want.view(np.uint8))
