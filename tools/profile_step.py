@@ -25,6 +25,9 @@ WL = {
     "c3d1_e4m3": ("e4m3", 65536, 32768, "L0", [], "SUM_DIM1", False),
     "c3d1_bf16": ("bf16", 32768, 32768, "L0", [], "SUM_DIM1", False),
     "var": ("f32", 1 << 30, 1, "L0", [], "VAR", False),
+    "var_bf16": ("bf16", 1 << 31, 1, "L0", [], "VAR", False),
+    "c3d1_f32": ("f32", 32768, 32768, "L0", [], "SUM_DIM1", False),
+    "c1g": ("f32", 1_000_000, 1, "S0 L0 MUL L1 ADD", [2.5], "ACCU", True),
     "imin": ("f32", 1 << 30, 1, "L0", [], "INDEX_MIN", False),
     "axpy": ("f32", 1 << 30, 1, "S0 L0 MUL L1 ADD", [2.5], "ACCU", True),
     "c3d0": ("f64", 32768, 32768, "L0", [], "SUM_DIM0", False),
