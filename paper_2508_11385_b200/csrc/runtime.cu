@@ -107,6 +107,7 @@ struct coot_ctx {
   bool tma_ctas_env = false;  // COOT_TMA_CTAS given (tuning runs): keep it as is
   int tma_tile_units = 0;   // TMA driver: units per operand tile override (0 = policy)
   int tma_smem_kb = 0;      // TMA driver: stage-ring budget override in KB (0 = policy)
+  int dim_ring_kb = 48;     // TMA dim kernels: stage-ring budget in KB (COOT_DIM_RING_KB)
   int dim_tma = 0;          // sum(X,dim): TMA-staged kernels when the layout allows
   int pdl = 1;              // programmatic dependent launch of fused / dim kernels
   int producer_sleep = -1;  // TMA producer sleeps on a full ring: -1 policy, 0 never, 1 always
@@ -850,7 +851,7 @@ coot_status run_dim(coot_ctx* ctx, const coot_expr* e, const Shape& sh, uint32_t
     d.seg_len = L;
     d.nseg = (uint32_t)S;
     const u64 stage_bytes = nk * coot::kTileUnits * 16;
-    const u64 stages = std::max<u64>(2, std::min<u64>(8, (96u << 10) / stage_bytes));
+    const u64 stages = std::max<u64>(2, std::min<u64>(16, ((u64)ctx->dim_ring_kb << 10) / stage_bytes));
     d.f.tile_units = coot::kTileUnits;
     d.f.stages = (uint32_t)stages;
     p.smem = pad_smem(ctx, (unsigned)(stages * stage_bytes + 16 * stages), ctx->tma_ctas_per_sm);
@@ -875,7 +876,7 @@ coot_status run_dim(coot_ctx* ctx, const coot_expr* e, const Shape& sh, uint32_t
     d.ccols = ccols;
     d.nchunks = (uint32_t)nchunks;
     const u64 stage_bytes = nk * cg * R1 * es;
-    const u64 stages = std::max<u64>(2, std::min<u64>(8, (96u << 10) / stage_bytes));
+    const u64 stages = std::max<u64>(2, std::min<u64>(16, ((u64)ctx->dim_ring_kb << 10) / stage_bytes));
     d.f.stages = (uint32_t)stages;
     p.smem = pad_smem(ctx, (unsigned)(stages * stage_bytes + 16 * stages), ctx->tma_ctas_per_sm);
     p.grid = (unsigned)std::min<u64>(nrt * nchunks, G);
@@ -1109,6 +1110,11 @@ coot_status coot_init(coot_ctx** out, int device, void* cuda_stream, uint32_t fl
   // dim sums default to the LDG kernels: measured faster on B200 (c3: dim0
   // 7.25 vs 7.04 TB/s, dim1 7.07 vs 6.74 TB/s)
   ctx->dim_tma = env_int("COOT_DIM_TMA", 0) ? 1 : 0;
+  // TMA dim kernels' ring: 48 KB (3 stages of 4 columns x 1024 f32 rows) per CTA,
+  // 2 CTAs per SM.  f32 sum(X,1) at 32768^2 (tools/gpu_r02o.sh, interleaved):
+  // 32 KB 6.48, 48 KB 6.92, 64 KB 6.75, 80 KB 6.47, 96 KB 6.30 TB/s; 3-4 CTAs
+  // per SM slower at every ring size
+  ctx->dim_ring_kb = std::max(32, std::min(200, env_int("COOT_DIM_RING_KB", 48)));
   // back-to-back calls overlap each launch with the previous kernel's tail
   // (COOT_PDL=0: plain stream-ordered launches)
   ctx->pdl = env_int("COOT_PDL", 1) ? 1 : 0;
