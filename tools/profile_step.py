@@ -25,6 +25,7 @@ WL = {
     "c3d1_e4m3": ("e4m3", 65536, 32768, "L0", [], "SUM_DIM1", False),
     "c3d1_bf16": ("bf16", 32768, 32768, "L0", [], "SUM_DIM1", False),
     "var": ("f32", 1 << 30, 1, "L0", [], "VAR", False),
+    "c2ro_f64": ("f64", 1 << 14, 1 << 15, "L0 L1 MUL EXP S0 L2 MUL ADD", [3.0], "ACCU", False),
     "var_bf16": ("bf16", 1 << 31, 1, "L0", [], "VAR", False),
     "c3d1_f32": ("f32", 32768, 32768, "L0", [], "SUM_DIM1", False),
     "c1g": ("f32", 1_000_000, 1, "S0 L0 MUL L1 ADD", [2.5], "ACCU", True),
