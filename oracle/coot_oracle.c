@@ -26,11 +26,9 @@
  *    (DESIGN.md "Input recipe"); fill::randu is uniform [0,1).
  *
  * Pins: every function here is pinned by tests/test_oracle_*.py.
- * Parity unpinned (corners, R6 / R12 / R13): f64 EXP / LOG inputs
- * whose result lies within 2^-98 of a rounding midpoint (binary128 cannot
- * decide all of them); f64 NORM2 beyond |v| > 1.3e154 or below 1e-154 (the
- * device's f64 squares overflow / underflow there, the oracle's long-double
- * squares do not); MIN / MAX with NaN inputs and the sign of a zero extreme.
+ * Parity unpinned (corners, R6 / R13): f64 EXP / LOG inputs whose
+ * result lies within 2^-98 of a rounding midpoint (binary128 cannot decide
+ * all of them); MIN / MAX with NaN inputs and the sign of a zero extreme.
  *
  * Build: gcc -O2 -ffp-contract=off -fno-fast-math -fPIC -shared (x86-64 SSE2,
  * FLT_EVAL_METHOD == 0) -lquadmath -lm.  See oracle/build.py.

@@ -1088,6 +1088,55 @@ __device__ __forceinline__ double sumsq_f64(const float (&x)[W]) {
   return r;
 }
 
+// f64 sums of squares over the whole f64 range (norm2, R12): value = s * 2^es
+// (es even).  Units whose squares are normal numbers well inside the range add
+// to s directly while es == 0 (the common case: one compare more than a plain
+// sum); any other unit (a square outside [2^-900, 2^900], huge or tiny values,
+// subnormals, non-finite) is squared after an exact power-of-two scaling by its
+// largest exponent and merged with exponent alignment, and a merged s above
+// 2^900 is renormalised — so neither a square nor the sum overflows or flushes
+// (an f64 norm2 of 1e200-sized data was inf; of 1e-200-sized data 0).
+__device__ __forceinline__ void sq_merge_scaled(double& s, int& es, double o, int eo) {
+  if (o == 0.0) return;
+  if (s == 0.0) {
+    s = o;
+    es = eo;
+  } else if (eo > es) {
+    s = __dadd_rn(scalbn(s, es - eo), o);
+    es = eo;
+  } else {
+    s = __dadd_rn(s, scalbn(o, eo - es));
+  }
+  if (s > 0x1p900 && s <= 1.7976931348623157e308) {  // keep the sum far from overflow
+    s = scalbn(s, -400);
+    es += 400;
+  }
+}
+// The scaled add of one f64 unit (W <= 2 values: v1 unused when w2 is false).
+// Arguments and result by value: a noinline callee taking the accumulator by
+// reference pins it to local memory in the hot loop (f64 norm2 7.2 -> 4.7 TB/s).
+struct SqAcc {
+  double s;
+  int es;
+};
+static __device__ __noinline__ SqAcc sq_add_scaled(double s, int es, double v0, double v1, bool w2) {
+  SqAcc r{s, es};
+  const double a0 = fabs(v0), a1 = w2 ? fabs(v1) : 0.0;
+  const double kMax = 1.7976931348623157e308;
+  if (!(a0 <= kMax) || !(a1 <= kMax)) {  // inf / NaN propagate: inf^2 = inf, NaN stays NaN
+    r.s = __dadd_rn(r.s, __fma_rn(v0, v0, w2 ? __dmul_rn(v1, v1) : 0.0));
+    return r;
+  }
+  int m = -2000;
+  if (a0 != 0.0) m = ilogb(a0) + 1;
+  if (a1 != 0.0) m = max(m, ilogb(a1) + 1);
+  if (m == -2000) return r;  // all zeros
+  // the unit's squares scaled by 2^-2m (the largest lies in [1/4, 1))
+  const double x0 = scalbn(v0, -m), x1 = w2 ? scalbn(v1, -m) : 0.0;
+  sq_merge_scaled(r.s, r.es, __fma_rn(x1, x1, __dmul_rn(x0, x0)), 2 * m);
+  return r;
+}
+
 // Per-thread / per-block / per-rank accumulator for every reduction kind.
 //  ACC_SUM, ACC_SUMSQ: s (f64 for floats, u64 modular for ints)
 //  ACC_MINMAX:         mn, mx
@@ -1105,8 +1154,10 @@ struct Accum {
   double c, s1, s2;
   float cf;  // VAR on f32 / 16-bit / 8-bit: the shift c as f32 (exact: c is an element)
   bool has;  // IMIN / IMAX: an element has been seen (hot-loop copy of idx != ~0)
+  int es;    // SUMSQ on f64: the sum is s * 2^es (sq_add_scaled)
   __device__ __forceinline__ void init() {
     s = S(0);
+    es = 0;
     mn = MinMaxId<T>::lo();
     mx = MinMaxId<T>::hi();
     n = 0;
@@ -1208,6 +1259,24 @@ struct Accum {
           s = sum_add<S>(s, (double)u);
         else
           s = sum_add<S>(s, sumsq_f64<W>(q));
+      } else if constexpr (std::is_same<T, double>::value) {
+        T q[W];
+#pragma unroll
+        for (int w = 0; w < W; ++w) q[w] = bin<COOT_OP_MUL>(v[w], v[w]);
+        const double u = unit_sum<T, W>(q);
+        bool zero = true;  // u == 0 from squares that flushed is not a zero unit
+#pragma unroll
+        for (int w = 0; w < W; ++w) zero = zero && (v[w] == 0.0);
+        // (a thread adds far fewer than 2^100 units of <= 2^901 each: s cannot
+        // overflow here; merges renormalise — no test on the s chain per unit)
+        if (__builtin_expect(es == 0 && ((u >= 0x1p-900 && u <= 0x1p900) || zero), 1)) {
+          s = __dadd_rn(s, u);
+        } else {
+          static_assert(W <= 2, "f64 units hold at most 2 elements");
+          const SqAcc r = sq_add_scaled(s, es, v[0], W > 1 ? v[W - 1] : 0.0, W > 1);
+          s = r.s;
+          es = r.es;
+        }
       } else {
         T q[W];
 #pragma unroll
@@ -1226,7 +1295,11 @@ struct Accum {
   __device__ __forceinline__ void warp_reduce() {
 #pragma unroll
     for (int m = 16; m >= 1; m >>= 1) {
-      if constexpr (ACC == ACC_SUM || ACC == ACC_SUMSQ) {
+      if constexpr (ACC == ACC_SUMSQ && std::is_same<T, double>::value) {
+        const double o = shfl_xor(s, m);
+        const int eo = __shfl_xor_sync(0xffffffffu, es, m);
+        sq_merge_scaled(s, es, o, eo);
+      } else if constexpr (ACC == ACC_SUM || ACC == ACC_SUMSQ) {
         s = sum_add<S>(s, shfl_xor(s, m));
       } else if constexpr (ACC == ACC_MINMAX) {
         mn = bin<COOT_OP_MIN>(mn, shfl_xor(mn, m));
@@ -1245,7 +1318,9 @@ struct Accum {
     }
   }
   __device__ __forceinline__ void merge(const Accum& o) {
-    if constexpr (ACC == ACC_SUM || ACC == ACC_SUMSQ) {
+    if constexpr (ACC == ACC_SUMSQ && std::is_same<T, double>::value) {
+      sq_merge_scaled(s, es, o.s, o.es);
+    } else if constexpr (ACC == ACC_SUM || ACC == ACC_SUMSQ) {
       s = sum_add<S>(s, o.s);
     } else if constexpr (ACC == ACC_MINMAX) {
       mn = bin<COOT_OP_MIN>(mn, o.mn);
@@ -1298,7 +1373,7 @@ struct Accum {
       r.b = idx;
     } else if constexpr (is_float<T>()) {
       r.a = (u64)__double_as_longlong((double)s);
-      r.b = 0;
+      r.b = (u64)(long long)es;  // 0 except for f64 SUMSQ (the scale exponent)
     } else {
       r.a = (u64)s;
       r.b = 0;
@@ -1321,6 +1396,7 @@ struct Accum {
       idx = r.b;
     } else if constexpr (is_float<T>()) {
       s = __longlong_as_double((long long)r.a);
+      if constexpr (ACC == ACC_SUMSQ && std::is_same<T, double>::value) es = (int)(long long)r.b;
     } else {
       s = r.a;
     }
@@ -1399,7 +1475,10 @@ __device__ __forceinline__ void write_final(const Accum<T, ACC>& acc, uint32_t k
       out[1] = as_result(acc.mx);
     }
   } else if constexpr (ACC == ACC_SUMSQ) {
-    out[0] = round_to<R>(__dsqrt_rn(acc.s));
+    if constexpr (std::is_same<T, double>::value)
+      out[0] = scalbn(__dsqrt_rn(acc.s), acc.es / 2);  // es is even: exact scaling
+    else
+      out[0] = round_to<R>(__dsqrt_rn(acc.s));
   } else if constexpr (ACC == ACC_SUM) {
     if constexpr (is_float<T>()) {
       out[0] = round_to<R>(acc.s);

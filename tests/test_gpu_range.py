@@ -1,4 +1,5 @@
-"""norm2 and var over the whole f32 / bf16 range (R12, R22).
+"""norm2 and var over the whole f32 / bf16 range, and f64 norm2 over the whole
+f64 range (R12, R22).
 
 The device squares f32 / bf16 values in f32 inside a 16-byte unit; a unit with
 an element (or, for var, a deviation from the shift) outside [2^-63, 2^62) is
@@ -110,3 +111,49 @@ def test_norm2_nonfinite(ctxs, etype):
         assert np.isinf(oracle.to_float(etype, gpu(ctx, etype, y, "NORM2"))[0]), name
         y[5001] = np.nan if etype == "f32" else oracle.half_from_double(etype, float("nan"))
         assert np.isnan(oracle.to_float(etype, gpu(ctx, etype, y, "NORM2"))[0]), name
+
+
+# ---- f64 norm2 over the whole f64 range (R12): scaled sum of squares -------
+@pytest.mark.parametrize("scale", [1e300, 2.0 ** 600, 1e154, 1e-154, 2.0 ** -600, 1e-300,
+                                   2.0 ** -1060, 1.0])
+@pytest.mark.parametrize("n", [1, 7, 100_003])
+def test_f64_norm2_whole_range(ctxs, scale, n):
+    """f64 squares of 1e300 overflow and of 1e-300 flush to 0; the scaled
+    accumulator (value = s 2^es) keeps norm2 within 1e-12 of the oracle's
+    long-double result, on every driver, down to subnormal inputs."""
+    check(ctxs, "f64", "NORM2", scaled("f64", n, scale, shift=0.5))
+
+
+def test_f64_norm2_isolated_outliers_and_shards(ctxs):
+    """Mostly in-range data with a few 1e250 / 1e-300 elements (those units and
+    the threads that saw them take the scaled path); also the rank-order
+    combine of shard partials carries the scale exponent."""
+    import paper_2508_11385_b200 as coot
+    x = scaled("f64", 300_007, 1.0, shift=0.25)
+    for i in (0, 5, 4096, 123_457, 300_006):
+        x[i] = 3e250
+    for i in (1, 77, 200_000):
+        x[i] = 1e-300
+    check(ctxs, "f64", "NORM2", x)
+    want = oracle.reduce("f64", "NORM2", x)
+    ctx = ctxs["tma"]
+    d = to_dev(x, "f64")
+    nparts = 5
+    parts = torch.zeros(nparts * 4, dtype=torch.int64, device="cuda")
+    for r in range(nparts):
+        b, e = coot.shard_range(x.size, r, nparts, 16)
+        ctx.reduce_partial("f64", e - b, 1, P("L0"), [d[b:e]], [], "NORM2", parts[4 * r:4 * r + 4])
+    res = torch.zeros(2, dtype=torch.float64, device="cuda")
+    ctx.combine("f64", "NORM2", parts, nparts, 1, res)
+    torch.cuda.synchronize()
+    assert_reduction(res[0].item(), want, "f64", "NORM2")
+
+
+def test_f64_norm2_nonfinite(ctxs):
+    x = scaled("f64", 10_001, 1e200)
+    for name, ctx in ctxs.items():
+        y = x.copy()
+        y[5000] = np.inf
+        assert np.isinf(gpu(ctx, "f64", y, "NORM2")[0]), name
+        y[5001] = np.nan
+        assert np.isnan(gpu(ctx, "f64", y, "NORM2")[0]), name

@@ -51,6 +51,7 @@ WL = {
     "var_2p30": ("f32", 1 << 30, 1, "L0", [], "VAR", False, False),
     "var_f64_2p29": ("f64", 1 << 29, 1, "L0", [], "VAR", False, False),
     "imin_2p30": ("f32", 1 << 30, 1, "L0", [], "INDEX_MIN", False, False),
+    "norm2_f64_2p29": ("f64", 1 << 29, 1, "L0", [], "NORM2", False, False),
     "diag_add_1e4": ("f32", 10_000, 1, "L0 S0 ADD", [100.0], None, "diag", False),
     "submat_axpy": ("f32", 8192, 8192, "S0 L0 MUL L1 ADD", [2.5], "ACCU", "submat", False),
     "bf16_c2_2p31": ("bf16", 1 << 31, 1, "L0 L1 MUL EXP S0 L2 MUL ADD", [3.0], "ACCU", False, False),
