@@ -28,7 +28,10 @@
  * Pins: every function here is pinned by tests/test_oracle_*.py.
  * Parity unpinned (corners, R6 / R13): f64 EXP / LOG inputs whose
  * result lies within 2^-98 of a rounding midpoint (binary128 cannot decide
- * all of them); MIN / MAX with NaN inputs and the sign of a zero extreme.
+ * all of them); f64 VAR / STDDEV whose squared deviations leave the f64 range
+ * (the device's shifted f64 squares overflow / flush there, the oracle's
+ * long-double ones do not); MIN / MAX with NaN inputs and the sign of a zero
+ * extreme.
  *
  * Build: gcc -O2 -ffp-contract=off -fno-fast-math -fPIC -shared (x86-64 SSE2,
  * FLT_EVAL_METHOD == 0) -lquadmath -lm.  See oracle/build.py.
