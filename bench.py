@@ -388,13 +388,17 @@ def measure_scaling_configs(coot, ctx, comm_ctx, mailbox, rank, world, dist, dev
             box = {}
             transports.append(("mailbox", lambda: box.__setitem__("r", mailbox.reduce(lw, kind, out=z)),
                                lambda: box["r"]))
-        for tname, call, get in transports:
+        # two interleaved rounds (A B A B), best per transport: the compute-heavy
+        # forms run at the power cap, so whichever went second lost clock
+        for tname, call, get in transports * 2:
             dist.barrier()
             torch.cuda.synchronize()
             ms, reps = time_calls(call, ctx.stream)
             tt = torch.tensor([ms], dtype=torch.float64, device=dev)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             ms = float(tt[0])
+            if tname in rec and rec[tname]["ms"] <= ms:
+                continue
             rec[tname] = {"ms": ms, "reps": reps, "GBps": n * bpe / (ms * 1e-3) / 1e9,
                           "elements_per_s": n / (ms * 1e-3)}
             if store != "inplace":  # in place: the data change every call
@@ -441,13 +445,15 @@ def measure_c3_dim1_scaling(coot, ctx, comm_ctx, mailbox, rank, world, dist, dev
         box = {}
         transports.append(("mailbox", lambda: box.__setitem__("r", mailbox.sum_dim1(lw)),
                            lambda: box["r"]))
-    for tname, call, get in transports:
+    for tname, call, get in transports * 2:  # interleaved rounds, best per transport
         dist.barrier()
         torch.cuda.synchronize()
         ms, reps = time_calls(call, ctx.stream)
         tt = torch.tensor([ms], dtype=torch.float64, device=dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms = float(tt[0])
+        if tname in rec and rec[tname]["ms"] <= ms:
+            continue
         rec[tname] = {"ms": ms, "reps": reps, "GBps": m * ncols * 8 / (ms * 1e-3) / 1e9}
         results[tname] = get().clone()
     if len(results) == 2:

@@ -91,13 +91,30 @@ __device__ void vec_exchange_finish(const DimArgs& d, uint32_t tid, uint32_t NT,
   }
   sync();
   const S* data = reinterpret_cast<const S*>(ex.mbox[ex.rank] + kVecMboxHeader) + half * d.vcap;
-  for (u64 r = tid; r < d.m; r += NT) {
-    S tot = S(0);
-    for (uint32_t q = 0; q < P; ++q) tot = sum_add<S>(tot, __ldcg(data + (u64)q * d.vcap + r));
-    R v;
-    if constexpr (is_float<T>()) v = round_to<R>(tot);
-    else v = (R)tot;
-    reinterpret_cast<R*>(d.result)[r] = v;
+  // one CTA combines all m rows, 8 rows per thread at a time so that their
+  // loads are in flight together (a rolled loop paid an L2 round trip per
+  // row); each row still sums q = 0..P-1 in order, as combine_vec_kernel
+  for (u64 r0 = tid; r0 < d.m; r0 += 8ull * NT) {
+    S tot[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) tot[k] = S(0);
+    for (uint32_t q = 0; q < P; ++q) {
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const u64 r = r0 + (u64)k * NT;
+        if (r < d.m) tot[k] = sum_add<S>(tot[k], __ldcg(data + (u64)q * d.vcap + r));
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const u64 r = r0 + (u64)k * NT;
+      if (r < d.m) {
+        R v;
+        if constexpr (is_float<T>()) v = round_to<R>(tot[k]);
+        else v = (R)tot[k];
+        reinterpret_cast<R*>(d.result)[r] = v;
+      }
+    }
   }
 }
 

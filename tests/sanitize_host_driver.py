@@ -83,6 +83,11 @@ def libcoot_host():
     if rc == 0:
         lib.coot_destroy(h)
     assert lib.coot_destroy(None) == 0  # NULL is a no-op (coot.h)
+    mb = (ctypes.c_void_p * 2)(None, None)
+    e = N.Expr()
+    for kind in (5, 6, 99):  # SUM_DIM0 / SUM_DIM1 / junk: rejected before any CUDA call
+        assert lib.coot_sum_dim_exchange(None, ctypes.byref(e), kind, mb, 2, 0, 1, 10, None) != 0
+    assert lib.coot_vec_mailbox_create(None, 0, None, None) != 0
     for fn, args in (("coot_sync", [None]), ("coot_stats", [None, None]),
                      ("coot_eval", [None, None, None]), ("coot_comm_destroy", [None])):
         assert getattr(lib, fn)(*args) != 0, fn

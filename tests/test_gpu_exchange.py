@@ -194,7 +194,7 @@ def _emulated_sum_dim1(ctx, vboxes, cap, elem, m, blocks, epoch):
     return results, comb.cpu()
 
 
-@pytest.mark.parametrize("nranks", [2, 3])
+@pytest.mark.parametrize("nranks", [1, 2, 3])
 @pytest.mark.parametrize("elem,m,ncols", [("f64", 1000, 301), ("f64", 4096, 2000),
                                           ("f32", 4096, 1203), ("bf16", 777, 64),
                                           ("u32", 1000, 37), ("e4m3", 2048, 100),
