@@ -1214,13 +1214,30 @@ struct Accum {
         // f32 / 16-bit: the unit's shifted sums in f32 (the shift is an element,
         // so exact in f32; x - c is exact when x is near c), widened to f64 once
         // per unit — relative error ~W * 2^-24, far inside the 1e-5 bar
-        float a1 = 0.f, a2 = 0.f, x[W];
-        widen_f32<T, W>(v, x);
+        float a1 = 0.f, a2 = 0.f;
+        if constexpr (is_narrow<T>() && W >= 2) {
+          // d = RN(x - c) straight from the 16-bit view (add.rn.f32.{bf16,f16}
+          // of -c: one FHADD instead of a widening and an FSUB, same bits)
 #pragma unroll
-        for (int w = 0; w < W; ++w) {
-          const float d = __fsub_rn(x[w], cf);
-          a1 = __fadd_rn(a1, d);
-          a2 = __fmaf_rn(d, d, a2);
+          for (int w = 0; w + 1 < W; w += 2) {
+            unsigned short h[2];
+            to_h16<T>({v[w], v[w + 1]}, h);
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+              const float d = add_f32_h16<T>(-cf, h[k]);
+              a1 = __fadd_rn(a1, d);
+              a2 = __fmaf_rn(d, d, a2);
+            }
+          }
+        } else {
+          float x[W];
+          widen_f32<T, W>(v, x);
+#pragma unroll
+          for (int w = 0; w < W; ++w) {
+            const float d = __fsub_rn(x[w], cf);
+            a1 = __fadd_rn(a1, d);
+            a2 = __fmaf_rn(d, d, a2);
+          }
         }
         if (__builtin_expect(!sq_range_checked<T>() || sq_sum_ok(a2), 1)) {
           s1 = __dadd_rn(s1, (double)a1);
@@ -1228,6 +1245,8 @@ struct Accum {
         } else {
           // squared deviations left f32's range (x - c or a square overflowed,
           // or all are tiny), or the unit equals the shift: shifted sums in f64
+          float x[W];
+          widen_f32<T, W>(v, x);
           double b1 = 0.0, b2 = 0.0;
 #pragma unroll
           for (int w = 0; w < W; ++w) {

@@ -251,6 +251,10 @@ struct CatalogEval<StaticProg<Code...>> {
 // compile-time indices.  LOAD takes its operand index at run time from the
 // source (a shared-memory address under the TMA driver).  One dispatch
 // evaluates UD whole 16-byte units.
+// EXP / LOG group size inside the interpreter (coot_device.cuh un_vec)
+#ifndef COOT_INTERP_EXP_GROUP
+#define COOT_INTERP_EXP_GROUP 4
+#endif
 #define COOT_KEY(op, d) ((op) * 9 + (d))
 // Fused-operand dispatch ops (host peephole, runtime.cu fill_program): an ADD,
 // SUB or MUL whose right operand is an operand load or a scalar, "L k OP" -> OP_L k and
@@ -287,7 +291,7 @@ struct InterpEval {
 #define COOT_UN_CASE(OP, d)                                                \
   case COOT_KEY(COOT_OP_##OP, d):                                          \
     if constexpr ((d) >= 1 && (d) <= SMAX && op_legal<T>(COOT_OP_##OP)) {  \
-      un_vec<COOT_OP_##OP, 4>(st[(d) >= 1 ? (d) - 1 : 0]);                 \
+      un_vec<COOT_OP_##OP, COOT_INTERP_EXP_GROUP>(st[(d) >= 1 ? (d) - 1 : 0]);   \
     } else if constexpr ((d) >= 1 && (d) <= SMAX) {                        \
       __trap(); /* op illegal for T: rejected on the host (R9) */          \
     }                                                                      \

@@ -60,6 +60,8 @@ WL = {
     "f16_c2_2p31": ("f16", 1 << 31, 1, "L0 L1 MUL EXP S0 L2 MUL ADD", [3.0], "ACCU", False, False),
     "f16_axpy_eval_2p30": ("f16", 1 << 30, 1, "S0 L0 MUL L1 ADD", [2.5], None, True, False),
     "bf16_var_2p31": ("bf16", 1 << 31, 1, "L0", [], "VAR", False, False),
+    "f16_var_2p31": ("f16", 1 << 31, 1, "L0", [], "VAR", False, False),
+    "e4m3_var_2p32": ("e4m3", 1 << 32, 1, "L0", [], "VAR", False, False),
     "bf16_norm2_2p31": ("bf16", 1 << 31, 1, "L0", [], "NORM2", False, False),
     "bf16_dim0": ("bf16", 32768, 32768, "L0", [], "SUM_DIM0", False, False),
     "bf16_dim1": ("bf16", 32768, 32768, "L0", [], "SUM_DIM1", False, False),
