@@ -619,10 +619,25 @@ def main():
                if multi and not share else None)
     comm_ctx = None
     if multi and not share:
-        uid = [coot.Context.comm_unique_id() if rank == 0 else None]
+        # libcoot's communicator; any failure (e.g. NCCL not loadable by
+        # libcoot) leaves every rank on the other transports
+        try:
+            uid = [coot.Context.comm_unique_id() if rank == 0 else None]
+        except Exception as exc:  # noqa: BLE001
+            sys.stderr.write(f"bench.py: coot_comm_unique_id failed: {exc}\n")
+            uid = [None]
         dist.broadcast_object_list(uid, src=0)
-        comm_ctx = coot.Context(local, stream=stream)
-        comm_ctx.comm_init(world, rank, uid[0], "cols")
+        if uid[0] is not None:
+            comm_ctx = coot.Context(local, stream=stream)
+            try:
+                comm_ctx.comm_init(world, rank, uid[0], "cols")
+            except Exception as exc:  # noqa: BLE001
+                sys.stderr.write(f"bench.py: coot_comm_init failed: {exc}\n")
+                comm_ctx = None
+            ok = torch.tensor([1 if comm_ctx is not None else 0], device=dev)
+            dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+            if int(ok.item()) == 0:
+                comm_ctx = None
     reducer = cdist.DistReducer(ctx) if multi else None
     if exchange == "mailbox" and mailbox is None:
         exchange = "nccl" if comm_ctx is not None else "torch"
