@@ -388,9 +388,9 @@ def measure_scaling_configs(coot, ctx, comm_ctx, mailbox, rank, world, dist, dev
             box = {}
             transports.append(("mailbox", lambda: box.__setitem__("r", mailbox.reduce(lw, kind, out=z)),
                                lambda: box["r"]))
-        # two interleaved rounds (A B A B), best per transport: the compute-heavy
-        # forms run at the power cap, so whichever went second lost clock
-        for tname, call, get in transports * 2:
+        # two rounds in opposite orders (A B B A), best per transport: the
+        # compute-heavy forms run at the power cap, so whichever went second lost clock
+        for tname, call, get in transports + transports[::-1]:
             dist.barrier()
             torch.cuda.synchronize()
             ms, reps = time_calls(call, ctx.stream)
@@ -445,7 +445,7 @@ def measure_c3_dim1_scaling(coot, ctx, comm_ctx, mailbox, rank, world, dist, dev
         box = {}
         transports.append(("mailbox", lambda: box.__setitem__("r", mailbox.sum_dim1(lw)),
                            lambda: box["r"]))
-    for tname, call, get in transports * 2:  # interleaved rounds, best per transport
+    for tname, call, get in transports + transports[::-1]:  # A B B A, best per transport
         dist.barrier()
         torch.cuda.synchronize()
         ms, reps = time_calls(call, ctx.stream)
