@@ -719,11 +719,19 @@ coot_status run_fused(coot_ctx* ctx, const coot_expr* e, const Shape& sh, int ac
   p.catalog = (ctx->flags & COOT_INIT_FORCE_INTERP) ? -1 : match_catalog(e);
   if (acc >= coot::ACC_VAR && p.catalog > 0) p.catalog = -1;  // see pick_fused_acc
   p.interp_large = (e->n_operands > 4 || sh.max_depth > 4) ? 1 : 0;
-  // shallow interpreter class (TMA driver, 4-byte types): a 2-slot stack, 4
+  // shallow interpreter class (TMA driver): a 2-slot stack, 4 (4-byte types)
   // units per dispatch (coot_launch.cuh pick_fused_acc)
+  // Every element size takes it except 16-/8-bit programs without EXP / LOG
+  // (tools/sweep.py, interleaved: f64 c2 +18 %, s64 c4 +11 %, bf16 c2 +18 %,
+  // E4M3 c2 +30 %, f16 axpy -4.5 %).
   static const bool no_shallow = env_int("COOT_NO_SHALLOW_INTERP", 0) != 0;  // A/B aid
-  if (p.catalog < 0 && !p.interp_large && p.driver == 1 && elem_size(e->elem) == 4 &&
-      fused_depth <= 2 && !no_shallow)
+  static const bool shallow_all = env_int("COOT_SHALLOW_ALL", 0) != 0;        // A/B aid
+  bool transcendental = false;
+  for (uint32_t i = 0; i < e->n_instr; ++i)
+    transcendental = transcendental || e->prog[i].op == COOT_OP_EXP || e->prog[i].op == COOT_OP_LOG;
+  const bool shallow_type = elem_size(e->elem) >= 4 || transcendental || shallow_all;
+  if (p.catalog < 0 && !p.interp_large && p.driver == 1 && shallow_type && fused_depth <= 2 &&
+      !no_shallow)
     p.interp_large = 2;
   u64 grid;
   if (p.driver == 1) {

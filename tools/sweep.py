@@ -72,6 +72,9 @@ WL = {
     "e5m2_axpy_eval_2p31": ("e5m2", 1 << 31, 1, "S0 L0 MUL L1 ADD", [2.5], None, True, False),
     "e4m3_dot_2p32": ("e4m3", 1 << 32, 1, "L0 L1 MUL", [], "ACCU", False, False),
     "e4m3_dim1": ("e4m3", 65536, 32768, "L0", [], "SUM_DIM1", False, False),
+    "s64_interp_c4": ("s64", 1 << 28, 1, "L0 L1 MUL S0 L2 MUL SUB", [7], "MINMAX", False, True),
+    "e4m3_interp_c2": ("e4m3", 1 << 31, 1, "L0 L1 MUL EXP S0 L2 MUL ADD", [3.0], "ACCU", True, True),
+    "f16_interp_axpy": ("f16", 1 << 30, 1, "S0 L0 MUL L1 ADD", [2.5], "ACCU", True, True),
     "bf16_interp_c2":("bf16", 1 << 30, 1, "L0 L1 MUL EXP S0 L2 MUL ADD", [3.0], "ACCU", True, True),
 }
 
